@@ -1,0 +1,197 @@
+/*
+ * magicdec_b200.h — C ABI of the B200 (sm_100a) MagicDec self-speculative decode hot path.
+ *
+ * MagicDec (arXiv 2408.11049) speeds up large-batch long-context decoding by letting
+ * the target model draft for itself with a StreamingLLM-compressed KV cache
+ * (attention-sink tokens + a recent window) and then
+ * verifying the gamma drafted tokens against the full KV cache.
+ * One speculation step is gamma draft passes plus one verify pass
+ * (T_total = gamma*T_D + T_V) followed by the speculative-sampling
+ * acceptance of Leviathan et al..  In the long-context, large-batch
+ * regime the paper targets, KV loading dominates both passes,
+ * so the four calls below are the data-parallel hot path:
+ *
+ *   md_kv_append          write the new K/V rows of a pass into the shared cache
+ *   md_draft_attn_sparse  1 query token / sequence over sink ∪ window (no KV copy)
+ *   md_verify_attn_full   gamma+1 query tokens / sequence over the full KV, GQA, causal
+ *   md_spec_accept        batched acceptance + residual / bonus resampling (or greedy)
+ *   md_philox_u32         counter-based uniforms feeding md_spec_accept
+ *
+ * Conventions shared by every call
+ *   - Every pointer argument named as "device" is caller-owned CUDA device memory;
+ *     the library never allocates, frees, synchronises or copies host<->device.
+ *     Each call only enqueues work on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream), so a whole speculation step can be captured in a CUDA graph, as the
+ *     paper does with PyTorch CUDA graphs.
+ *   - bf16 tensors are raw IEEE bfloat16 bit patterns (uint16_t storage).
+ *   - GQA: query head h reads KV head floor(h / g), g = num_q_heads / num_kv_heads.
+ *   - Softmax scale `scale` multiplies q.k (pass 1/sqrt(head_dim) for the usual model).
+ *   - LSE outputs are natural-log log-sum-exp of the scaled scores.
+ *   - Return value: MD_OK, or an error code with a message from md_last_error().
+ *     Host-side argument errors are detected before anything is enqueued.  Violating a
+ *     device-side precondition (values inside device arrays) is undefined behaviour.
+ *   - Thread safety: calls are reentrant; the only library state is the thread-local
+ *     error string.
+ */
+#ifndef MAGICDEC_B200_H
+#define MAGICDEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MD_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define MD_API __attribute__((visibility("default")))
+#else
+#define MD_API
+#endif
+
+typedef struct CUstream_st* md_stream_t; /* identical to cudaStream_t */
+
+typedef enum {
+  MD_OK = 0,
+  MD_ERR_INVALID_ARG = 1, /* bad scalar, NULL or misaligned pointer, bad stride      */
+  MD_ERR_UNSUPPORTED = 2, /* valid but not built: head_dim not in {64,128}, g*T > 64  */
+  MD_ERR_WORKSPACE = 3,   /* workspace NULL or smaller than md_attn_workspace_bytes   */
+  MD_ERR_CUDA = 4         /* a CUDA runtime/driver call or kernel launch failed       */
+} md_status;
+
+typedef enum { MD_ACCEPT_SAMPLE = 0, MD_ACCEPT_GREEDY = 1 } md_accept_mode;
+
+/*
+ * One layer's KV cache, shared by the draft and the verify passes (the paper's "static
+ * compressed KV" of P:720 is realised as an index set over this cache, not a copy).
+ * k, v: device bf16, logical shape [batch][num_kv_heads][capacity][head_dim], element
+ * strides (stride_b, stride_h, stride_s, 1).  Strides must be multiples of 8 elements
+ * (16 bytes) and k, v 16-byte aligned.  The contiguous layout is
+ * (num_kv_heads*capacity*head_dim, capacity*head_dim, head_dim); an NHD cache
+ * ([batch][capacity][num_kv_heads][head_dim]) is expressed with
+ * (capacity*Hkv*d, d, Hkv*d).  Passed by pointer, read during the call only.
+ */
+typedef struct {
+  void* k;
+  void* v;
+  int32_t batch, num_kv_heads, head_dim, capacity;
+  int64_t stride_b, stride_h, stride_s;
+} md_kv_cache;
+
+/* MD_ABI_VERSION of the loaded library. */
+MD_API int md_abi_version(void);
+
+/* Message for the last non-MD_OK status returned on this thread ("" if none).
+ * Valid until the next md_* call on the same thread. */
+MD_API const char* md_last_error(void);
+
+/*
+ * md_kv_append — cache update of one pass (implied by decode,
+ * P:720; ragged per-sequence positions).
+ * For every sequence b, new token t in [0, T) and KV head h:
+ *     cache[b][h][start_pos[b] + t][:] = new[b][t][h][:]     (for k and v)
+ * k_new, v_new: device bf16 [B][T][Hkv][head_dim], contiguous (as a QKV projection
+ * emits them, already rotary-embedded upstream).  start_pos: device int32[B].
+ * A draft step appends T = 1 row at L_b + j; verify appends T = gamma+1 rows at L_b,
+ * overwriting the draft-written slots (reading Z11).
+ * Preconditions (device): 0 <= start_pos[b] and start_pos[b] + T <= capacity.
+ */
+MD_API md_status md_kv_append(const md_kv_cache* cache, const void* k_new, const void* v_new, int32_t T,
+                       const int32_t* start_pos, md_stream_t stream);
+
+/*
+ * Bytes of scratch the attention calls need for split-KV partials.
+ * `max_kv_len` is the largest per-sequence number of keys the call will read: the
+ * verify call's max_kv_len, or min(sink + window, capacity) for the draft call.  The
+ * value depends on the current device's SM count; query it on the device you launch on.
+ * Returns 0 for invalid arguments (and when no scratch is needed).
+ */
+MD_API size_t md_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads, int32_t head_dim,
+                               int32_t T, int32_t max_kv_len);
+
+/*
+ * md_verify_attn_full — verification attention ("the time taken by the target
+ * model to verify gamma tokens"; "verification and decoding share the same KV
+ * budget"; reading Z4: T = gamma + 1 query tokens, the pending token plus gamma drafts).
+ * For b < B, t < T, h < Hq, with n = kv_len[b] (which COUNTS the T new tokens):
+ *     J        = [0, n - T + t]                     (causal among the T new rows, Z10)
+ *     out[b][t][h][:] = softmax_j(scale * q[b][t][h] . k[b][h/g][j]) @ v[b][h/g][J]
+ *     lse[b][t][h]    = log sum_{j in J} exp(scale * q . k_j)
+ * The g*T query rows of one KV head share a single read of that head's KV.
+ * T = 1 is plain autoregressive decode.
+ *   q:   device bf16 [B][T][Hq][head_dim], contiguous.   kv_len: device int32[B].
+ *   max_kv_len: host upper bound on kv_len[b] (used to plan splits; keys beyond
+ *               kv_len[b] are never read).
+ *   out: device fp32 [B][T][Hq][head_dim]; lse: device fp32 [B][T][Hq] or NULL.
+ *   workspace: device scratch of >= md_attn_workspace_bytes(B, Hq, Hkv, d, T, max_kv_len)
+ *              bytes (may be NULL when that is 0).
+ * Supported: head_dim in {64, 128}, g*T <= 64, 1 <= T <= 16.
+ * Preconditions (device): T <= kv_len[b] <= min(max_kv_len, capacity).
+ */
+MD_API md_status md_verify_attn_full(const md_kv_cache* cache, const void* q, int32_t num_q_heads, int32_t T,
+                              const int32_t* kv_len, int32_t max_kv_len, float scale, float* out, float* lse,
+                              void* workspace, size_t workspace_bytes, md_stream_t stream);
+
+/*
+ * md_draft_attn_sparse — self-speculative draft attention over the StreamingLLM
+ * compressed KV ("StreamingLLM style sparse KV for drafting", P:460 budgets,
+ * P:720 static compressed KV; Eq.3 P:1081 with T_select = 0 for a static method).
+ * For b < B, h < Hq, with n = kv_len[b] (counts the just-appended draft token):
+ *     J = {j < min(sink, n)}  U  {max(sink, n - window) <= j < n}     (no index twice)
+ *     out[b][h][:] = softmax_j(scale * q[b][h] . k[b][h/g][j]) @ v[b][h/g][J],  lse likewise.
+ * The window slides with n (reading Z2); positions are not re-indexed (Z3); the
+ * kernel walks the two row ranges of the shared cache directly (no gather copy).
+ *   q: device bf16 [B][Hq][head_dim]; out: fp32 [B][Hq][head_dim]; lse: fp32 [B][Hq] or NULL.
+ *   workspace: >= md_attn_workspace_bytes(B, Hq, Hkv, d, 1, min(sink + window, capacity)).
+ * Supported: head_dim in {64, 128}, g <= 64, sink >= 0, window >= 0, sink + window >= 1.
+ * Preconditions (device): 1 <= kv_len[b] <= capacity.
+ */
+MD_API md_status md_draft_attn_sparse(const md_kv_cache* cache, const void* q, int32_t num_q_heads, const int32_t* kv_len,
+                               int32_t sink, int32_t window, float scale, float* out, float* lse, void* workspace,
+                               size_t workspace_bytes, md_stream_t stream);
+
+/*
+ * md_philox_u32 — Philox4x32-10 uniforms for md_spec_accept (
+ * SPEC.md S:472 counter-based PRNG with per-sequence streams; reading Z8).
+ * out[b][w] = word (w % 4) of Philox4x32-10(counter = (b, step_lo, step_hi, w / 4),
+ *                                          key = (seed_lo, seed_hi)).
+ * out: device uint32 [B][words_per_seq].  For md_spec_accept use words_per_seq = gamma+2.
+ */
+MD_API md_status md_philox_u32(uint64_t seed, uint64_t step, int32_t B, int32_t words_per_seq, uint32_t* out,
+                        md_stream_t stream);
+
+/*
+ * md_spec_accept — batched speculative-sampling acceptance (the rule of Leviathan et
+ * al. that P:204 cites; accepted counts are ragged per sequence; the paper's
+ * experiments decode greedily).  Per sequence b (j = 0..gamma-1, x = d[b][j]):
+ *   SAMPLE: accept iff (rnd[b][j] >> 3) * q[b][j][x] < p[b][j][x] * 2^29, evaluated
+ *           exactly in fp64 (Z6).  At the first rejection n = j, draw the new token
+ *           from W = max(0, floor(p_n 2^40) - floor(q_n 2^40)) (if sum W = 0: W =
+ *           floor(p_n 2^40); if that is 0 too: lowest-index argmax p_n) with the
+ *           64-bit uniform u = rnd[b][gamma] << 32 | rnd[b][gamma+1]:
+ *           t = floor(u * sum W / 2^64), token = min{k : sum_{i<=k} W_i > t} (Z7, Z8).
+ *           If all gamma are accepted, n = gamma and the bonus token is drawn the
+ *           same way from W = floor(p_gamma 2^40).
+ *   GREEDY: accept iff argmax p[b][j] == x (lowest index on ties); new token =
+ *           argmax p[b][n].  rnd and q are not read (may be NULL).
+ * Outputs: out_tokens[b] = [d_0 .. d_{n-1}, new, -1 ...] (gamma+1 entries),
+ * num_accepted[b] = n, and, if committed_len_inout != NULL, committed_len[b] += n + 1.
+ * Integer decisions are exact, so results are bit-reproducible and equal to the
+ * oracle's on the same inputs.  gamma = 0 samples one token from p[b][0] (plain AR).
+ *   p: device fp32 [B][gamma+1][V]; q: device fp32 [B][gamma][V];
+ *   draft_tokens: device int32 [B][gamma]; rnd: device uint32 [B][gamma+2];
+ *   out_tokens: device int32 [B][gamma+1]; num_accepted: device int32 [B].
+ * Supported: 0 <= gamma <= 15, V >= 1.
+ * Preconditions (device): 0 <= d < V; probabilities finite and in [0, 1].
+ */
+MD_API md_status md_spec_accept(const float* p, const float* q, const int32_t* draft_tokens, const uint32_t* rnd,
+                         int32_t B, int32_t gamma, int32_t V, md_accept_mode mode, int32_t* out_tokens,
+                         int32_t* num_accepted, int32_t* committed_len_inout, md_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MAGICDEC_B200_H */

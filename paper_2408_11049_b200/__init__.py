@@ -1,0 +1,161 @@
+"""paper_2408_11049_b200 — thin Python binding of the MagicDec B200 C ABI.
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels of
+`libmagicdec_b200.so` (declared in include/magicdec_b200.h).  PyTorch is used for
+device memory and streams.  There is no CPU fallback: a missing library or a CPU
+tensor raises.
+
+Functions mirror the C calls (same names without the `md_` prefix):
+    kv_append, attn_workspace_bytes, verify_attn_full, draft_attn_sparse,
+    philox_u32, spec_accept
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmagicdec_b200.so")
+
+MD_OK, MD_ERR_INVALID_ARG, MD_ERR_UNSUPPORTED, MD_ERR_WORKSPACE, MD_ERR_CUDA = 0, 1, 2, 3, 4
+MD_ACCEPT_SAMPLE, MD_ACCEPT_GREEDY = 0, 1
+
+# the symbols include/magicdec_b200.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_workspace_bytes",
+               "md_verify_attn_full", "md_draft_attn_sparse", "md_philox_u32", "md_spec_accept")
+
+
+class MDError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"md status {status}: {msg}")
+        self.status = status
+
+
+class KVCache(ctypes.Structure):
+    """md_kv_cache: caller-owned [B][Hkv][cap][d] bf16 K and V with element strides."""
+    _fields_ = [("k", ctypes.c_void_p), ("v", ctypes.c_void_p),
+                ("batch", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("capacity", ctypes.c_int32),
+                ("stride_b", ctypes.c_int64), ("stride_h", ctypes.c_int64), ("stride_s", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load the CUDA library (raises if it has not been built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -m paper_2408_11049_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    c_void_p, i32, i64, f32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
+    u64 = ctypes.c_uint64
+    pc = ctypes.POINTER(KVCache)
+    lib.md_abi_version.restype = ctypes.c_int
+    lib.md_last_error.restype = ctypes.c_char_p
+    lib.md_kv_append.argtypes = [pc, c_void_p, c_void_p, i32, c_void_p, c_void_p]
+    lib.md_attn_workspace_bytes.argtypes = [i32, i32, i32, i32, i32, i32]
+    lib.md_attn_workspace_bytes.restype = sz
+    lib.md_verify_attn_full.argtypes = [pc, c_void_p, i32, i32, c_void_p, i32, f32, c_void_p, c_void_p,
+                                        c_void_p, sz, c_void_p]
+    lib.md_draft_attn_sparse.argtypes = [pc, c_void_p, i32, c_void_p, i32, i32, f32, c_void_p, c_void_p,
+                                         c_void_p, sz, c_void_p]
+    lib.md_philox_u32.argtypes = [u64, u64, i32, i32, c_void_p, c_void_p]
+    lib.md_spec_accept.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, i32, i32, i32, ctypes.c_int,
+                                   c_void_p, c_void_p, c_void_p, c_void_p]
+    for name in ("md_kv_append", "md_verify_attn_full", "md_draft_attn_sparse", "md_philox_u32", "md_spec_accept"):
+        getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != MD_OK:
+        raise MDError(status, _lib.md_last_error().decode())
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("md tensors must be CUDA tensors (no CPU fallback)")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def make_cache(k: torch.Tensor, v: torch.Tensor) -> KVCache:
+    """md_kv_cache from two [B, Hkv, cap, d] bf16 views (any strides with unit last stride)."""
+    if k.shape != v.shape or k.stride() != v.stride() or k.dtype != torch.bfloat16 or v.dtype != torch.bfloat16:
+        raise ValueError("k and v caches must be bf16 with identical shapes and strides")
+    if k.dim() != 4 or k.stride(3) != 1:
+        raise ValueError("cache must be [B, Hkv, cap, d] with unit stride on d")
+    B, H, cap, d = k.shape
+    return KVCache(_ptr(k), _ptr(v), B, H, d, cap, k.stride(0), k.stride(1), k.stride(2))
+
+
+def abi_version() -> int:
+    return load_library().md_abi_version()
+
+
+def kv_append(k_cache, v_cache, k_new, v_new, start_pos, stream=None):
+    """cache[b, h, start_pos[b] + t] = new[b, t, h] for K and V; new is [B, T, Hkv, d]."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    T = k_new.shape[1]
+    _check(lib.md_kv_append(ctypes.byref(c), _ptr(k_new.contiguous()), _ptr(v_new.contiguous()), T,
+                            _ptr(start_pos), _stream(stream)))
+
+
+def attn_workspace_bytes(batch, num_q_heads, num_kv_heads, head_dim, T, max_kv_len) -> int:
+    return int(load_library().md_attn_workspace_bytes(batch, num_q_heads, num_kv_heads, head_dim, T, max_kv_len))
+
+
+def _ws(workspace):
+    if workspace is None:
+        return None, 0
+    return _ptr(workspace), workspace.numel() * workspace.element_size()
+
+
+def verify_attn_full(q, k_cache, v_cache, kv_len, max_kv_len, scale, out, lse=None, workspace=None, stream=None):
+    """q [B, T, Hq, d] bf16 -> out [B, T, Hq, d] fp32 (and lse [B, T, Hq] fp32)."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_verify_attn_full(ctypes.byref(c), _ptr(q), q.shape[2], q.shape[1], _ptr(kv_len), int(max_kv_len),
+                                   float(scale), _ptr(out), _ptr(lse), ws, wsb, _stream(stream)))
+
+
+def draft_attn_sparse(q, k_cache, v_cache, kv_len, sink, window, scale, out, lse=None, workspace=None, stream=None):
+    """q [B, Hq, d] bf16 over the sink + window rows -> out [B, Hq, d] fp32 (and lse [B, Hq])."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_draft_attn_sparse(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(kv_len), int(sink), int(window),
+                                    float(scale), _ptr(out), _ptr(lse), ws, wsb, _stream(stream)))
+
+
+def philox_u32(seed, step, out, stream=None):
+    """out [B, words] uint32 (torch.int32 storage) <- Philox4x32-10 words."""
+    lib = load_library()
+    _check(lib.md_philox_u32(int(seed) & (2**64 - 1), int(step) & (2**64 - 1), out.shape[0], out.shape[1],
+                             _ptr(out), _stream(stream)))
+
+
+def spec_accept(p, q, draft_tokens, rnd, out_tokens, num_accepted, committed_len=None, mode="sample",
+                stream=None):
+    """Batched acceptance.  p [B, gamma+1, V] fp32, q [B, gamma, V] fp32, draft_tokens [B, gamma] int32,
+    rnd [B, gamma+2] (int32 storage of uint32) -> out_tokens [B, gamma+1], num_accepted [B]."""
+    lib = load_library()
+    B, G1, V = p.shape
+    m = MD_ACCEPT_SAMPLE if mode == "sample" else MD_ACCEPT_GREEDY
+    _check(lib.md_spec_accept(_ptr(p), _ptr(q), _ptr(draft_tokens), _ptr(rnd), B, G1 - 1, V, m, _ptr(out_tokens),
+                              _ptr(num_accepted), _ptr(committed_len), _stream(stream)))

@@ -1,0 +1,58 @@
+// kv_append.cu — md_kv_append: scatter the new K/V rows of a pass into the shared cache
+// (SURVEY §8(a) row a1).  Pure bandwidth: one thread moves one 16-byte vector, the
+// source [B][T][Hkv][d] is read fully coalesced and each destination row (d bf16 =
+// 128/256 B) is written contiguously.
+#include "md_internal.h"
+
+namespace md {
+
+__global__ void __launch_bounds__(256) kv_append_kernel(uint16_t* __restrict__ kc, uint16_t* __restrict__ vc,
+                                                        const uint16_t* __restrict__ kn,
+                                                        const uint16_t* __restrict__ vn,
+                                                        const int32_t* __restrict__ start, int T, int Hkv, int d,
+                                                        int64_t sB, int64_t sH, int64_t sS, int64_t nvec) {
+  const int vec_per_row = d >> 3;  // 8 bf16 per 16-byte vector
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / vec_per_row;  // row of [B][T][Hkv]
+    const int c = static_cast<int>(i - row * vec_per_row) << 3;
+    const int h = static_cast<int>(row % Hkv);
+    const int64_t bt = row / Hkv;
+    const int t = static_cast<int>(bt % T);
+    const int b = static_cast<int>(bt / T);
+    const int64_t dst = b * sB + h * sH + (int64_t)(__ldg(start + b) + t) * sS + c;
+    const uint4 kv = __ldg(reinterpret_cast<const uint4*>(kn + row * d + c));
+    const uint4 vv = __ldg(reinterpret_cast<const uint4*>(vn + row * d + c));
+    *reinterpret_cast<uint4*>(kc + dst) = kv;
+    *reinterpret_cast<uint4*>(vc + dst) = vv;
+  }
+}
+
+}  // namespace md
+
+extern "C" md_status md_kv_append(const md_kv_cache* c, const void* k_new, const void* v_new, int32_t T,
+                                  const int32_t* start_pos, md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(c != nullptr && k_new != nullptr && v_new != nullptr && start_pos != nullptr, MD_ERR_INVALID_ARG,
+             "md_kv_append: NULL argument");
+  MD_REQUIRE(c->k != nullptr && c->v != nullptr, MD_ERR_INVALID_ARG, "md_kv_append: NULL cache pointer");
+  MD_REQUIRE(c->batch >= 1 && c->num_kv_heads >= 1 && c->capacity >= 1 && T >= 1, MD_ERR_INVALID_ARG,
+             "md_kv_append: batch, num_kv_heads, capacity and T must be >= 1");
+  MD_REQUIRE(c->head_dim >= 8 && c->head_dim % 8 == 0, MD_ERR_INVALID_ARG,
+             "md_kv_append: head_dim must be a positive multiple of 8");
+  MD_REQUIRE(T <= c->capacity, MD_ERR_INVALID_ARG, "md_kv_append: T exceeds capacity");
+  MD_REQUIRE(c->stride_b % 8 == 0 && c->stride_h % 8 == 0 && c->stride_s % 8 == 0, MD_ERR_INVALID_ARG,
+             "md_kv_append: cache strides must be multiples of 8 elements");
+  MD_REQUIRE(aligned16(c->k) && aligned16(c->v) && aligned16(k_new) && aligned16(v_new), MD_ERR_INVALID_ARG,
+             "md_kv_append: pointers must be 16-byte aligned");
+  const int64_t nvec = (int64_t)c->batch * T * c->num_kv_heads * (c->head_dim / 8);
+  const int threads = 256;
+  int64_t blocks = (nvec + threads - 1) / threads;
+  const int64_t cap_blocks = (int64_t)device_sm_count() * 16;
+  if (blocks > cap_blocks) blocks = cap_blocks;
+  kv_append_kernel<<<static_cast<unsigned>(blocks), threads, 0, (cudaStream_t)stream>>>(
+      static_cast<uint16_t*>(c->k), static_cast<uint16_t*>(c->v), static_cast<const uint16_t*>(k_new),
+      static_cast<const uint16_t*>(v_new), start_pos, T, c->num_kv_heads, c->head_dim, c->stride_b, c->stride_h,
+      c->stride_s, nvec);
+  return check_launch("md_kv_append");
+}

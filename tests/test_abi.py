@@ -1,0 +1,83 @@
+"""CPU checks of the C-ABI boundary: the library loads, exports every symbol the header
+declares, and rejects bad host-side arguments before touching a GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2408_11049_b200 as md
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "magicdec_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(md_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_documented_calls():
+    assert set(declared_symbols()) == set(md.ABI_SYMBOLS)
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    lib = md.load_library()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert lib.md_abi_version() == 1
+
+
+def test_only_the_abi_is_exported():
+    """The .so exports the md_* C entry points (plus static-cudart internals); no C++ API."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", md.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
+    assert set(md.ABI_SYMBOLS) <= exported
+    assert not any(s.startswith("_ZN2md") for s in exported)
+
+
+def _cache(d=128, stride_s=128):
+    return md.KVCache(16, 16, 2, 2, d, 64, 2 * 64 * stride_s, 64 * stride_s, stride_s)
+
+
+def _err(status):
+    return status, md.load_library().md_last_error().decode()
+
+
+def test_host_side_validation_without_gpu():
+    lib = md.load_library()
+    c = _cache(d=96)
+    st, msg = _err(lib.md_verify_attn_full(ctypes.byref(c), 16, 4, 5, 16, 64, 0.1, 16, None, None, 0, None))
+    assert st == md.MD_ERR_UNSUPPORTED and "head_dim" in msg
+    c = _cache()
+    st, msg = _err(lib.md_verify_attn_full(ctypes.byref(c), 16, 4, 17, 16, 64, 0.1, 16, None, None, 0, None))
+    assert st == md.MD_ERR_UNSUPPORTED and "T must be" in msg
+    st, msg = _err(lib.md_verify_attn_full(ctypes.byref(c), 16, 3, 5, 16, 64, 0.1, 16, None, None, 0, None))
+    assert st == md.MD_ERR_INVALID_ARG and "multiple" in msg
+    st, msg = _err(lib.md_verify_attn_full(ctypes.byref(c), 16, 64, 5, 16, 64, 0.1, 16, None, None, 0, None))
+    assert st == md.MD_ERR_UNSUPPORTED and "64" in msg               # g*T = 32*5 rows
+    c = _cache(stride_s=132)
+    st, msg = _err(lib.md_draft_attn_sparse(ctypes.byref(c), 16, 4, 16, 4, 60, 0.1, 16, None, None, 0, None))
+    assert st == md.MD_ERR_INVALID_ARG and "stride" in msg
+    c = _cache()
+    st, msg = _err(lib.md_draft_attn_sparse(ctypes.byref(c), 16, 4, 16, 0, 0, 0.1, 16, None, None, 0, None))
+    assert st == md.MD_ERR_INVALID_ARG and "sink" in msg
+    st, _ = _err(lib.md_spec_accept(16, 16, 16, 16, 4, 16, 32, 0, 16, 16, None, None))
+    assert st == md.MD_ERR_UNSUPPORTED
+    st, _ = _err(lib.md_spec_accept(16, None, 16, 16, 4, 3, 32, 0, 16, 16, None, None))
+    assert st == md.MD_ERR_INVALID_ARG
+    st, _ = _err(lib.md_kv_append(ctypes.byref(c), None, 16, 1, 16, None))
+    assert st == md.MD_ERR_INVALID_ARG
+
+
+def test_workspace_query_is_host_only():
+    assert md.attn_workspace_bytes(64, 32, 8, 128, 5, 32773) >= 0
+    assert md.attn_workspace_bytes(64, 32, 8, 96, 5, 32773) == 0
+    assert md.attn_workspace_bytes(2, 4, 4, 64, 1, 64) == 0        # a single split needs no scratch
+
+
+def test_cpu_tensor_is_rejected():
+    import torch
+    with pytest.raises(ValueError):
+        md._ptr(torch.zeros(4))

@@ -1,0 +1,41 @@
+"""The CUDA input generator (synth/csrc) is bit-identical to the numpy one (synth/__init__.py)."""
+import numpy as np
+import pytest
+import torch
+
+import synth as S
+import synth.cuda as SC
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(t):
+    return t.cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+@pytest.mark.parametrize("regime", [S.FLAT, S.Regime("peaky", sink=4, needle_period=37)])
+def test_cache_generator_bit_exact(regime):
+    B, H, cap, d = 3, 4, 300, 128
+    k = torch.zeros((B, H, cap, d), dtype=torch.bfloat16, device="cuda")
+    SC.fill_cache(k, 11, S.T_KCACHE, 0, 250, regime)
+    SC.fill_cache(k, 11, S.T_KCACHE, 250, 50, regime)
+    ref = S.k_to_bf16_bits(S.kv_cache_k(11, S.T_KCACHE, B, H, d, 0, cap, regime=regime))
+    assert np.array_equal(_bits(k), ref)
+    # strided (NHD) destination
+    v = torch.zeros((B, cap, H, d), dtype=torch.bfloat16, device="cuda").permute(0, 2, 1, 3)
+    SC.fill_cache(v, 11, S.T_VCACHE, 0, cap, regime)
+    ref = S.k_to_bf16_bits(S.kv_cache_k(11, S.T_VCACHE, B, H, d, 0, cap, regime=regime))
+    assert np.array_equal(_bits(v.contiguous()), ref)
+
+
+@pytest.mark.parametrize("regime", [S.FLAT, S.Regime("peaky")])
+def test_query_and_new_kv_generators_bit_exact(regime):
+    q = torch.empty((3, 5, 32, 128), dtype=torch.bfloat16, device="cuda")
+    SC.fill_q(q, 4, S.T_QVERIFY, 8, regime)
+    assert np.array_equal(_bits(q), S.k_to_bf16_bits(S.q_rows_k(4, S.T_QVERIFY, 3, 5, 32, 8, 128, regime=regime)))
+    qd = torch.empty((3, 28, 128), dtype=torch.bfloat16, device="cuda")
+    SC.fill_q(qd, 4, S.T_QDRAFT, 4, regime)
+    assert np.array_equal(_bits(qd), S.k_to_bf16_bits(S.q_rows_k(4, S.T_QDRAFT, 3, 1, 28, 4, 128, regime=regime))[:, 0])
+    kn = torch.empty((3, 5, 8, 128), dtype=torch.bfloat16, device="cuda")
+    SC.fill_new_kv(kn, 4, S.T_KNEW)
+    assert np.array_equal(_bits(kn), S.k_to_bf16_bits(S.new_kv_k(4, S.T_KNEW, 3, 5, 8, 128)))
