@@ -193,8 +193,8 @@ def run_gpu(args):
     lse_v = torch.empty((B, T, Hq), device=dev)
     out_d = torch.empty((B, Hq, d), device=dev)
     lse_d = torch.empty((B, Hq), device=dev)
-    ws_v = torch.empty(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, T, max_kv)), dtype=torch.uint8, device=dev)
-    ws_d = torch.empty(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, min(sink + window, cap))),
+    ws_v = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, T, max_kv)), dtype=torch.uint8, device=dev)
+    ws_d = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, min(sink + window, cap))),
                        dtype=torch.uint8, device=dev)
     split_v = md.attn_workspace_bytes(B, Hq, Hkv, d, T, max_kv) > 0
     split_d = md.attn_workspace_bytes(B, Hq, Hkv, d, 1, min(sink + window, cap)) > 0
@@ -315,7 +315,7 @@ def run_gpu(args):
         kv_len_ar = kv_len_d
         out_a = torch.empty((B, 1, Hq, d), device=dev)
         lse_a = torch.empty((B, 1, Hq), device=dev)
-        ws_a = torch.empty(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, max_kv)), dtype=torch.uint8, device=dev)
+        ws_a = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, max_kv)), dtype=torch.uint8, device=dev)
         qa = qv[:, :1].contiguous()
         ar_ms = time_calls(lambda r: md.verify_attn_full(qa, kc[r % R], vc[r % R], kv_len_ar, max_kv, scale, out_a,
                                                          lse_a, ws_a)) * layers
@@ -333,32 +333,61 @@ def run_gpu(args):
                layers * (h_qv.nbytes + h_kv.nbytes + h_vv.nbytes) + h_p.nbytes + h_q.nbytes + h_d.nbytes)
         d2h = h_out.nbytes + h_n.nbytes
 
+        # Copies run on their own streams, double-buffered per call, so the H2D traffic of
+        # call c+2 overlaps the kernels of call c (a serving loop would prefetch the same way).
+        copy_s, pq_s = torch.cuda.Stream(), torch.cuda.Stream()
+        st_d = [(torch.empty_like(qd), torch.empty_like(knew_d), torch.empty_like(vnew_d)) for _ in range(2)]
+        st_v = [(torch.empty_like(qv), torch.empty_like(knew_v), torch.empty_like(vnew_v)) for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
+        pq_ready, acc_done = torch.cuda.Event(), torch.cuda.Event()
+        ncalls = gamma * layers + layers
+
+        def issue_copy(c):
+            sl = c % 2
+            with torch.cuda.stream(copy_s):
+                copy_s.wait_event(done[sl])
+                dst, src = (st_d[sl], (h_qd, h_kd, h_vd)) if c < gamma * layers else (st_v[sl], (h_qv, h_kv, h_vv))
+                for x, y in zip(dst, src):
+                    x.copy_(y, non_blocking=True)
+                ready[sl].record(copy_s)
+
         def e2e_step(i):
+            cur = torch.cuda.current_stream()
+            with torch.cuda.stream(pq_s):
+                pq_s.wait_event(acc_done)
+                p_t.copy_(h_p, non_blocking=True)
+                q_t.copy_(h_q, non_blocking=True)
+                dtok.copy_(h_d, non_blocking=True)
+                pq_ready.record(pq_s)
+            issue_copy(0)
+            issue_copy(1)
             torch.add(committed[None, :], ar, out=pos_buf)
-            for j in range(gamma):
-                for l in range(layers):
-                    kb, vb_ = kc[l % R], vc[l % R]
-                    qd.copy_(h_qd, non_blocking=True)
-                    knew_d.copy_(h_kd, non_blocking=True)
-                    vnew_d.copy_(h_vd, non_blocking=True)
-                    md.kv_append(kb, vb_, knew_d, vnew_d, pos_buf[j])
-                    md.draft_attn_sparse(qd, kb, vb_, pos_buf[j + 1], sink, window, scale, out_d, lse_d, ws_d)
+            for c in range(ncalls):
+                sl = c % 2
+                cur.wait_event(ready[sl])
+                l = c % layers
+                kb, vb_ = kc[l % R], vc[l % R]
+                if c < gamma * layers:
+                    j = c // layers
+                    q_, k_, v_ = st_d[sl]
+                    md.kv_append(kb, vb_, k_, v_, pos_buf[j])
+                    md.draft_attn_sparse(q_, kb, vb_, pos_buf[j + 1], sink, window, scale, out_d, lse_d, ws_d)
                     if world > 1:
                         gather_heads(out_d, world, buf=gath_d)
-            for l in range(layers):
-                kb, vb_ = kc[l % R], vc[l % R]
-                qv.copy_(h_qv, non_blocking=True)
-                knew_v.copy_(h_kv, non_blocking=True)
-                vnew_v.copy_(h_vv, non_blocking=True)
-                md.kv_append(kb, vb_, knew_v, vnew_v, pos_buf[0])
-                md.verify_attn_full(qv, kb, vb_, pos_buf[gamma + 1], max_kv, scale, out_v, lse_v, ws_v)
-                if world > 1:
-                    gather_heads(out_v, world, buf=gath_v)
-            p_t.copy_(h_p, non_blocking=True)
-            q_t.copy_(h_q, non_blocking=True)
-            dtok.copy_(h_d, non_blocking=True)
+                else:
+                    q_, k_, v_ = st_v[sl]
+                    md.kv_append(kb, vb_, k_, v_, pos_buf[0])
+                    md.verify_attn_full(q_, kb, vb_, pos_buf[gamma + 1], max_kv, scale, out_v, lse_v, ws_v)
+                    if world > 1:
+                        gather_heads(out_v, world, buf=gath_v)
+                done[sl].record(cur)
+                if c + 2 < ncalls:
+                    issue_copy(c + 2)
+            cur.wait_event(pq_ready)
             md.philox_u32(SEED, i, rnd)
             md.spec_accept(p_t, q_t, dtok, rnd, out_tok, nacc, committed, mode="sample")
+            acc_done.record(cur)
             h_out.copy_(out_tok, non_blocking=True)
             h_n.copy_(nacc, non_blocking=True)
 

@@ -107,6 +107,10 @@ MD_API md_status md_kv_append(const md_kv_cache* cache, const void* k_new, const
  * verify call's max_kv_len, or min(sink + window, capacity) for the draft call.  The
  * value depends on the current device's SM count; query it on the device you launch on.
  * Returns 0 for invalid arguments (and when no scratch is needed).
+ * The workspace holds split partials and per-(b, kv head) arrival counters: it must be
+ * zero-filled ONCE when allocated (e.g. cudaMemset / torch.zeros); every call leaves the
+ * counters at zero again, so it can be reused by any later call on the same stream
+ * (not by two calls in flight concurrently).
  */
 MD_API size_t md_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads, int32_t head_dim,
                                int32_t T, int32_t max_kv_len);

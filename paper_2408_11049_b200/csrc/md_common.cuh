@@ -100,3 +100,29 @@ MD_DEV float ex2(float x) {
 MD_DEV uint32_t swz128(int r, int c) { return static_cast<uint32_t>(r * 128 + ((c ^ (r & 7)) << 4)); }
 
 }  // namespace md
+
+namespace md {
+// 1-D bulk copy global -> shared (16-byte aligned, size multiple of 16), completing on an mbarrier.
+MD_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+}  // namespace md
+
+namespace md {
+// Transpose an 8x8 b16 matrix held in the standard mma fragment layout across the warp
+// (thread (g, c) holds row g, columns 2c..2c+1  ->  row g of the transpose).
+MD_DEV uint32_t movmatrix_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+// Release-add / acquire for the cross-CTA split-arrival counter (one thread per CTA).
+MD_DEV int atomic_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+}  // namespace md

@@ -4,9 +4,9 @@
 // products (m * q < p * 2^29, m = rnd >> 3: 29 x 24 bits fit in the 53-bit mantissa),
 // then draws the final token from an integer weight vector on the 2^-40 grid with a
 // 64-bit uniform.  All sums are uint64 (<= V * 2^40 < 2^58), so the result does not
-// depend on the reduction order and is bit-identical to the oracle's.  The locate
-// step is two-level: per-warp segment sums, a prefix over warps, then one warp
-// rescans its segment 32 entries at a time with a warp-inclusive scan.
+// depend on the reduction order and is bit-identical to the oracle's.  Each thread owns
+// a contiguous slice of the vocabulary row (8-deep batched loads); a block exclusive scan
+// of the slice sums locates the slice holding the draw, which one thread rescans.
 #include "md_common.cuh"
 #include "md_internal.h"
 
@@ -66,30 +66,130 @@ __device__ __forceinline__ uint64_t weight(const float* __restrict__ prow, const
   return P > Q ? P - Q : 0ull;
 }
 
-__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 struct Smem {
   uint64_t wsum[ACC_WARPS];
-  uint64_t wpre[ACC_WARPS];
+  uint64_t total;
   float amax_v[ACC_WARPS];
   int amax_i[ACC_WARPS];
-  uint64_t total;
   int token;
   int n;
 };
+
+// Thread tid owns the contiguous slice [tid*chunk, min(V, (tid+1)*chunk)) of the row, so
+// an exclusive scan of the per-thread sums gives every slice's starting prefix and the
+// locate step is one thread rescanning one slice.  Loads are batched 8 deep per thread
+// (memory-level parallelism; the row is read once from HBM).
+constexpr int UNR = 8;
+
+__device__ __forceinline__ uint64_t slice_sum(const float* __restrict__ prow, const float* __restrict__ qrow, int beg,
+                                              int end) {
+  uint64_t acc = 0;
+  int i = beg;
+  for (; i + UNR <= end; i += UNR) {
+    float pv[UNR], qv[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) pv[u] = __ldg(prow + i + u);
+    if (qrow != nullptr) {
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) qv[u] = __ldg(qrow + i + u);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const uint64_t P = grid40(pv[u]);
+      const uint64_t Q = qrow != nullptr ? grid40(qv[u]) : 0ull;
+      acc += P > Q ? P - Q : 0ull;
+    }
+  }
+  for (; i < end; ++i) acc += weight(prow, qrow, i);
+  return acc;
+}
+
+// Per-thread slice sums -> exclusive prefix (returned) and the block total in sm.total.
+__device__ uint64_t block_weight_scan(const float* prow, const float* qrow, int V, int chunk, Smem& sm,
+                                      uint64_t& mine) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int beg = min(V, tid * chunk), end = min(V, beg + chunk);
+  mine = slice_sum(prow, qrow, beg, end);
+  uint64_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t up = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += up;
+  }
+  __syncthreads();
+  if (lane == 31) sm.wsum[warp] = incl;
+  __syncthreads();
+  uint64_t before = 0, total = 0;
+  for (int w = 0; w < ACC_WARPS; ++w) {
+    const uint64_t v = sm.wsum[w];
+    if (w < warp) before += v;
+    total += v;
+  }
+  if (tid == 0) sm.total = total;
+  return before + incl - mine;
+}
+
+// token = min{k : sum_{i<=k} W_i > t}: the one thread whose slice straddles t rescans it.
+__device__ int block_locate(const float* prow, const float* qrow, int V, int chunk, uint64_t t, uint64_t pre,
+                            uint64_t mine, Smem& sm) {
+  const int tid = threadIdx.x;
+  if (mine != 0 && pre <= t && t < pre + mine) {
+    const int beg = tid * chunk, end = min(V, beg + chunk);
+    uint64_t run = pre;
+    int i = beg;
+    for (; i + UNR <= end; i += UNR) {
+      uint64_t w[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) w[u] = weight(prow, qrow, i + u);
+      uint64_t blk = 0;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) blk += w[u];
+      if (run + blk > t) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          run += w[u];
+          if (run > t) {
+            sm.token = i + u;
+            break;
+          }
+        }
+        i = end + 1;  // found
+        break;
+      }
+      run += blk;
+    }
+    for (; i < end; ++i) {
+      run += weight(prow, qrow, i);
+      if (run > t) {
+        sm.token = i;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  return sm.token;
+}
 
 // Lowest-index argmax of a row (block-wide).  All threads return the same value.
 __device__ int block_argmax(const float* __restrict__ row, int V, Smem& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float bv = -INFINITY;
   int bi = 0x7fffffff;
-  for (int i = tid; i < V; i += ACC_THREADS) {
+  int i = tid;
+  for (; i + (UNR - 1) * ACC_THREADS < V; i += UNR * ACC_THREADS) {
+    float v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) v[u] = __ldg(row + i + u * ACC_THREADS);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (v[u] > bv) {  // indices increase with u: strict > keeps the lowest index on ties
+        bv = v[u];
+        bi = i + u * ACC_THREADS;
+      }
+  }
+  for (; i < V; i += ACC_THREADS) {
     const float v = __ldg(row + i);
-    if (v > bv || (v == bv && i < bi)) {
+    if (v > bv) {
       bv = v;
       bi = i;
     }
@@ -111,62 +211,13 @@ __device__ int block_argmax(const float* __restrict__ row, int V, Smem& sm) {
   __syncthreads();
   if (tid == 0) {
     float v = sm.amax_v[0];
-    int i = sm.amax_i[0];
+    int idx = sm.amax_i[0];
     for (int w = 1; w < ACC_WARPS; ++w)
-      if (sm.amax_v[w] > v || (sm.amax_v[w] == v && sm.amax_i[w] < i)) {
+      if (sm.amax_v[w] > v || (sm.amax_v[w] == v && sm.amax_i[w] < idx)) {
         v = sm.amax_v[w];
-        i = sm.amax_i[w];
+        idx = sm.amax_i[w];
       }
-    sm.token = (i == 0x7fffffff) ? 0 : i;
-  }
-  __syncthreads();
-  return sm.token;
-}
-
-// Per-warp segment sums of the weights; returns the block total (all threads).
-__device__ uint64_t block_weight_sum(const float* prow, const float* qrow, int V, int seg, Smem& sm) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int beg = warp * seg, end = min(V, beg + seg);
-  uint64_t acc = 0;
-  for (int i = beg + lane; i < end; i += 32) acc += weight(prow, qrow, i);
-  acc = warp_sum_u64(acc);
-  __syncthreads();
-  if (lane == 0) sm.wsum[warp] = acc;
-  __syncthreads();
-  if (tid == 0) {
-    uint64_t run = 0;
-    for (int w = 0; w < ACC_WARPS; ++w) {
-      sm.wpre[w] = run;
-      run += sm.wsum[w];
-    }
-    sm.total = run;
-  }
-  __syncthreads();
-  return sm.total;
-}
-
-// token = min{k : sum_{i<=k} W_i > t}, given the segment sums from block_weight_sum.
-__device__ int block_locate(const float* prow, const float* qrow, int V, int seg, uint64_t t, Smem& sm) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t pre = sm.wpre[warp], ws = sm.wsum[warp];
-  if (ws != 0 && pre <= t && t < pre + ws) {  // exactly one warp satisfies this
-    const int beg = warp * seg, end = min(V, beg + seg);
-    uint64_t run = pre;
-    for (int base = beg; base < end; base += 32) {
-      const int i = base + lane;
-      uint64_t incl = (i < end) ? weight(prow, qrow, i) : 0ull;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t up = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += up;
-      }
-      const unsigned hit = __ballot_sync(0xffffffffu, run + incl > t);
-      if (hit) {
-        if (lane == 0) sm.token = base + __ffs(hit) - 1;
-        break;
-      }
-      run += __shfl_sync(0xffffffffu, incl, 31);
-    }
+    sm.token = (idx == 0x7fffffff) ? 0 : idx;
   }
   __syncthreads();
   return sm.token;
@@ -181,7 +232,7 @@ __global__ void __launch_bounds__(ACC_THREADS) spec_accept_kernel(
   const int64_t Vl = V;
   const float* pb = p + (int64_t)b * (gamma + 1) * Vl;
   const int32_t* db = dtok + (int64_t)b * gamma;
-  const int seg = ((V + ACC_WARPS - 1) / ACC_WARPS + 31) & ~31;
+  const int chunk = (V + ACC_THREADS - 1) / ACC_THREADS;
   int n, token;
   if (mode == MD_ACCEPT_SAMPLE) {
     const uint32_t* rb = rnd + (int64_t)b * (gamma + 2);
@@ -201,17 +252,22 @@ __global__ void __launch_bounds__(ACC_THREADS) spec_accept_kernel(
     n = sm.n;
     const float* prow = pb + (int64_t)n * Vl;
     const float* qrow = (n < gamma) ? q + ((int64_t)b * gamma + n) * Vl : nullptr;
-    uint64_t total = block_weight_sum(prow, qrow, V, seg, sm);
+    uint64_t mine;
+    uint64_t pre = block_weight_scan(prow, qrow, V, chunk, sm, mine);
+    __syncthreads();
+    uint64_t total = sm.total;
     if (total == 0 && qrow != nullptr) {  // degenerate residual: fall back to p (reading Z7)
       qrow = nullptr;
-      total = block_weight_sum(prow, qrow, V, seg, sm);
+      pre = block_weight_scan(prow, qrow, V, chunk, sm, mine);
+      __syncthreads();
+      total = sm.total;
     }
     if (total == 0) {
       token = block_argmax(prow, V, sm);  // invalid all-tiny row
     } else {
       const uint64_t u = (static_cast<uint64_t>(__ldg(rb + gamma)) << 32) | __ldg(rb + gamma + 1);
       const uint64_t t = __umul64hi(u, total);
-      token = block_locate(prow, qrow, V, seg, t, sm);
+      token = block_locate(prow, qrow, V, chunk, t, pre, mine, sm);
     }
   } else {
     n = gamma;

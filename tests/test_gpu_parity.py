@@ -31,7 +31,7 @@ def _run_verify(case: AttnCase, max_kv_len=None):
     out = torch.full((B, T, Hq, d), float("nan"), device="cuda")
     lse = torch.full((B, T, Hq), float("nan"), device="cuda")
     wsb = md.attn_workspace_bytes(B, Hq, case.Hkv, d, T, mkl)
-    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(wsb, 1), dtype=torch.uint8, device="cuda")
     md.verify_attn_full(case.qv, case.k, case.v, case.kv_len_t, mkl, case.scale, out, lse, ws)
     torch.cuda.synchronize()
     return out.cpu().numpy(), lse.cpu().numpy()
@@ -42,7 +42,7 @@ def _run_draft(case: AttnCase, sink, window):
     out = torch.full((B, Hq, d), float("nan"), device="cuda")
     lse = torch.full((B, Hq), float("nan"), device="cuda")
     wsb = md.attn_workspace_bytes(B, Hq, case.Hkv, d, 1, min(sink + window, case.cap))
-    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(wsb, 1), dtype=torch.uint8, device="cuda")
     md.draft_attn_sparse(case.qd, case.k, case.v, case.kv_len_t, sink, window, case.scale, out, lse, ws)
     torch.cuda.synchronize()
     return out.cpu().numpy(), lse.cpu().numpy()
@@ -235,3 +235,53 @@ def test_determinism_bitwise():
     c = _run_draft(case, 4, 1020)
     d = _run_draft(case, 4, 1020)
     assert np.array_equal(c[0], d[0]) and np.array_equal(c[1], d[1])
+
+
+def test_calls_are_graph_capturable():
+    """Every md_* call only enqueues work (no sync / alloc): a whole step captured in a CUDA
+    graph and replayed gives bit-identical results to eager execution (P:722 uses graphs)."""
+    case = AttnCase(4, 32, 8, 128, 2100, [2000, 1999, 1500, 700], T=5, seed=31).to_cuda()
+    B, T, Hq, d = 4, 5, 32, 128
+    mkl = 2090
+    out_v = torch.zeros((B, T, Hq, d), device="cuda")
+    out_d = torch.zeros((B, Hq, d), device="cuda")
+    ws_v = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, 8, d, T, mkl)), dtype=torch.uint8, device="cuda")
+    ws_d = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, 8, d, 1, 1024)), dtype=torch.uint8, device="cuda")
+    kn = torch.zeros((B, T, 8, d), dtype=torch.bfloat16, device="cuda")
+    start = torch.tensor([1995, 1994, 1495, 695], dtype=torch.int32, device="cuda")
+    p, q, dt, rnd = _accept_inputs(B, 4, 500, 1.0, seed=2)
+    pt, qt, dtt = torch.from_numpy(p).cuda(), torch.from_numpy(q).cuda(), torch.from_numpy(dt).cuda()
+    rt = torch.empty((B, 6), dtype=torch.int32, device="cuda")
+    ot = torch.empty((B, 5), dtype=torch.int32, device="cuda")
+    nt = torch.empty(B, dtype=torch.int32, device="cuda")
+
+    def step():
+        md.kv_append(case.k, case.v, kn, kn, start)
+        md.draft_attn_sparse(case.qd, case.k, case.v, case.kv_len_t, 4, 1020, case.scale, out_d, None, ws_d)
+        md.verify_attn_full(case.qv, case.k, case.v, case.kv_len_t, mkl, case.scale, out_v, None, ws_v)
+        md.philox_u32(5, 1, rt)
+        md.spec_accept(pt, qt, dtt, rt, ot, nt)
+
+    step()
+    torch.cuda.synchronize()
+    ref = [x.clone() for x in (out_v, out_d, ot, nt)]
+    for x in (out_v, out_d):
+        x.zero_()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            step()
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(ref, (out_v, out_d, ot, nt)):
+        assert torch.equal(a, b)
+
+
+def test_verify_max_gamma_and_rows():
+    """gamma = 15 (T = 16, the ABI maximum) with g = 4 -> 64 rows per KV head."""
+    case = AttnCase(2, 16, 4, 128, 400, [400, 77], T=16, seed=41).to_cuda()
+    o, l = _run_verify(case)
+    ro, rl = OA.verify_attn_full(case.qv_bits, case.k_bits, case.v_bits, case.kv_len, case.scale)
+    _cmp(o, l, ro, rl)

@@ -43,11 +43,11 @@ def test_fullsize_sampled_parity(name, B, Hq, Hkv, d, ctx, gamma, sink, window):
     out_v = torch.empty((B, T, Hq, d), device="cuda")
     lse_v = torch.empty((B, T, Hq), device="cuda")
     mkl = int(kv_v.max())
-    ws = torch.empty(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, T, mkl)), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, T, mkl)), dtype=torch.uint8, device="cuda")
     md.verify_attn_full(qv, k, v, torch.from_numpy(kv_v).cuda(), mkl, scale, out_v, lse_v, ws)
     out_d = torch.empty((B, Hq, d), device="cuda")
     lse_d = torch.empty((B, Hq), device="cuda")
-    wsd = torch.empty(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, min(sink + window, cap))),
+    wsd = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, min(sink + window, cap))),
                       dtype=torch.uint8, device="cuda")
     md.draft_attn_sparse(qd, k, v, torch.from_numpy(kv_d).cuda(), sink, window, scale, out_d, lse_d, wsd)
     torch.cuda.synchronize()

@@ -40,8 +40,8 @@ out_v = torch.empty((B, T, Hq, d), device="cuda")
 lse_v = torch.empty((B, T, Hq), device="cuda")
 out_d = torch.empty((B, Hq, d), device="cuda")
 lse_d = torch.empty((B, Hq), device="cuda")
-ws_v = torch.empty(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, T, mkl)), dtype=torch.uint8, device="cuda")
-ws_d = torch.empty(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, sink + window)), dtype=torch.uint8, device="cuda")
+ws_v = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, T, mkl)), dtype=torch.uint8, device="cuda")
+ws_d = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, sink + window)), dtype=torch.uint8, device="cuda")
 for i in range(ncalls):
     md.verify_attn_full(qv, kc[i % R], vc[i % R], kvv, mkl, scale, out_v, lse_v, ws_v)
 for i in range(ncalls):
