@@ -196,8 +196,6 @@ def run_gpu(args):
     ws_v = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, T, max_kv)), dtype=torch.uint8, device=dev)
     ws_d = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, min(sink + window, cap))),
                        dtype=torch.uint8, device=dev)
-    split_v = md.attn_workspace_bytes(B, Hq, Hkv, d, T, max_kv) > 0
-    split_d = md.attn_workspace_bytes(B, Hq, Hkv, d, 1, min(sink + window, cap)) > 0
     gath_v = torch.empty((world, B, T, Hq, d), device=dev) if world > 1 else None
     gath_d = torch.empty((world, B, Hq, d), device=dev) if world > 1 else None
 
@@ -218,7 +216,8 @@ def run_gpu(args):
             if world > 1:
                 gather_heads(out_v, world, buf=gath_v)
 
-    launches_per_step = gamma * layers * (2 + int(split_d)) + layers * (2 + int(split_v)) + 2
+    # per layer-call: md_kv_append + one attention kernel (stream-K, merge fused); + philox + accept
+    launches_per_step = gamma * layers * 2 + layers * 2 + 2
 
     # positions for the step are one plumbing op on the committed lengths
     pos_buf = torch.empty((gamma + 2, B), dtype=torch.int32, device=dev)
@@ -439,7 +438,7 @@ def run_gpu(args):
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "hbm", "achieved": round(v_gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(v_gbs / peak, 4), "traffic": traffic,
-                         "kernel": "md_verify_attn_full (attn_split_kernel + attn_merge_kernel)",
+                         "kernel": "md_verify_attn_full (attn_rows_kernel, stream-K persistent, fused split merge)",
                          "algorithmic_bytes_per_launch": vb, "ms_per_launch": round(v_ms, 4),
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
             "verify_gbs": round(v_gbs, 1),

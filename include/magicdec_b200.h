@@ -102,15 +102,13 @@ MD_API md_status md_kv_append(const md_kv_cache* cache, const void* k_new, const
                        const int32_t* start_pos, md_stream_t stream);
 
 /*
- * Bytes of scratch the attention calls need for split-KV partials.
- * `max_kv_len` is the largest per-sequence number of keys the call will read: the
- * verify call's max_kv_len, or min(sink + window, capacity) for the draft call.  The
- * value depends on the current device's SM count; query it on the device you launch on.
- * Returns 0 for invalid arguments (and when no scratch is needed).
- * The workspace holds split partials and per-(b, kv head) arrival counters: it must be
- * zero-filled ONCE when allocated (e.g. cudaMemset / torch.zeros); every call leaves the
- * counters at zero again, so it can be reused by any later call on the same stream
- * (not by two calls in flight concurrently).
+ * Bytes of scratch the attention calls need: per-CTA split partials
+ * (o, lse) of the units that straddle two CTAs of the persistent stream-K grid, and one
+ * arrival counter per (b, kv head).  Depends on (B, Hkv, g*T, head_dim) and the current
+ * device's SM count, not on the context length (`max_kv_len` is accepted for symmetry).
+ * The workspace must be zero-filled ONCE when allocated (e.g. cudaMemset / torch.zeros);
+ * every call leaves the counters at zero again, so it can be reused by any later call on
+ * the same stream (not by two calls in flight concurrently).  Returns 0 for invalid args.
  */
 MD_API size_t md_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads, int32_t head_dim,
                                int32_t T, int32_t max_kv_len);
@@ -129,8 +127,8 @@ MD_API size_t md_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_
  *   max_kv_len: host upper bound on kv_len[b] (used to plan splits; keys beyond
  *               kv_len[b] are never read).
  *   out: device fp32 [B][T][Hq][head_dim]; lse: device fp32 [B][T][Hq] or NULL.
- *   workspace: device scratch of >= md_attn_workspace_bytes(B, Hq, Hkv, d, T, max_kv_len)
- *              bytes (may be NULL when that is 0).
+ *   workspace: zero-initialised device scratch of >= md_attn_workspace_bytes(B, Hq, Hkv, d, T,
+ *              max_kv_len) bytes.
  * Supported: head_dim in {64, 128}, g*T <= 64, 1 <= T <= 16.
  * Preconditions (device): T <= kv_len[b] <= min(max_kv_len, capacity).
  */
@@ -148,7 +146,7 @@ MD_API md_status md_verify_attn_full(const md_kv_cache* cache, const void* q, in
  * The window slides with n (reading Z2); positions are not re-indexed (Z3); the
  * kernel walks the two row ranges of the shared cache directly (no gather copy).
  *   q: device bf16 [B][Hq][head_dim]; out: fp32 [B][Hq][head_dim]; lse: fp32 [B][Hq] or NULL.
- *   workspace: >= md_attn_workspace_bytes(B, Hq, Hkv, d, 1, min(sink + window, capacity)).
+ *   workspace: zero-initialised, >= md_attn_workspace_bytes(B, Hq, Hkv, d, 1, min(sink + window, capacity)).
  * Supported: head_dim in {64, 128}, g <= 64, sink >= 0, window >= 0, sink + window >= 1.
  * Preconditions (device): 1 <= kv_len[b] <= capacity.
  */

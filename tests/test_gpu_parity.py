@@ -285,3 +285,61 @@ def test_verify_max_gamma_and_rows():
     o, l = _run_verify(case)
     ro, rl = OA.verify_attn_full(case.qv_bits, case.k_bits, case.v_bits, case.kv_len, case.scale)
     _cmp(o, l, ro, rl)
+
+
+def test_stream_k_single_unit_spans_every_cta():
+    """B=1, one KV head: the single unit's tiles are spread over the whole persistent grid,
+    so its output is the merge of ~G partials (O6 across CTAs)."""
+    case = AttnCase(1, 4, 1, 128, 40000, [39999], T=5, seed=51).to_cuda()
+    o, l = _run_verify(case)
+    ro, rl = OA.verify_attn_full(case.qv_bits, case.k_bits, case.v_bits, case.kv_len, case.scale)
+    _cmp(o, l, ro, rl)
+    o, l = _run_draft(case, 4, 30000)
+    ro, rl = OA.draft_attn_sparse(case.qd_bits, case.k_bits, case.v_bits, case.kv_len, 4, 30000, case.scale)
+    _cmp(o, l, ro, rl)
+
+
+def test_stream_k_many_ragged_units():
+    """Many short ragged units: CTA ranges cut units at arbitrary tiles and a CTA spans
+    several units; lengths straddle tile boundaries (63/64/65) and equal T."""
+    rng = np.random.default_rng(61)
+    lens = rng.integers(5, 700, size=40)
+    lens[:6] = [5, 63, 64, 65, 128, 129]
+    case = AttnCase(40, 16, 2, 64, 704, lens, T=5, seed=61).to_cuda()
+    o, l = _run_verify(case)
+    ro, rl = OA.verify_attn_full(case.qv_bits, case.k_bits, case.v_bits, case.kv_len, case.scale)
+    _cmp(o, l, ro, rl)
+    o, l = _run_draft(case, 4, 100)
+    ro, rl = OA.draft_attn_sparse(case.qd_bits, case.k_bits, case.v_bits, case.kv_len, 4, 100, case.scale)
+    _cmp(o, l, ro, rl)
+
+
+def test_workspace_reuse_across_calls():
+    """The arrival counters are left at zero: back-to-back calls of different shapes on one
+    zero-initialised workspace stay correct."""
+    a = AttnCase(3, 32, 8, 128, 3000, [3000, 1700, 900], T=5, seed=71).to_cuda()
+    b = AttnCase(2, 8, 8, 128, 5000, [5000, 4999], T=4, seed=72).to_cuda()
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device="cuda")
+    for case, T in ((a, 5), (b, 4), (a, 5), (b, 4)):
+        out = torch.empty((case.B, T, case.Hq, case.d), device="cuda")
+        lse = torch.empty((case.B, T, case.Hq), device="cuda")
+        md.verify_attn_full(case.qv, case.k, case.v, case.kv_len_t, int(case.kv_len.max()), case.scale, out, lse, ws)
+        od = torch.empty((case.B, case.Hq, case.d), device="cuda")
+        md.draft_attn_sparse(case.qd, case.k, case.v, case.kv_len_t, 4, 1020, case.scale, od, None, ws)
+        torch.cuda.synchronize()
+        ro, rl = OA.verify_attn_full(case.qv_bits, case.k_bits, case.v_bits, case.kv_len, case.scale)
+        _cmp(out.cpu().numpy(), lse.cpu().numpy(), ro, rl)
+
+
+def test_large_batch_uses_global_walk():
+    """B > 1024 sequences (the in-CTA prefix table's limit): the CTA-range lookup falls back
+    to walking kv_len in global memory."""
+    rng = np.random.default_rng(81)
+    lens = rng.integers(4, 150, size=1030)
+    case = AttnCase(1030, 4, 1, 64, 152, lens, T=3, seed=81).to_cuda()
+    o, l = _run_verify(case)
+    ro, rl = OA.verify_attn_full(case.qv_bits, case.k_bits, case.v_bits, case.kv_len, case.scale)
+    _cmp(o, l, ro, rl)
+    o, l = _run_draft(case, 4, 60)
+    ro, rl = OA.draft_attn_sparse(case.qd_bits, case.k_bits, case.v_bits, case.kv_len, 4, 60, case.scale)
+    _cmp(o, l, ro, rl)
