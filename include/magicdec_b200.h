@@ -13,6 +13,7 @@
  *
  *   md_kv_append          write the new K/V rows of a pass into the shared cache
  *   md_draft_attn_sparse  1 query token / sequence over sink ∪ window (no KV copy)
+ *   md_draft_attn_indexed 1 query token / sequence over a SnapKV index list ∪ recent tail
  *   md_verify_attn_full   gamma+1 query tokens / sequence over the full KV, GQA, causal
  *   md_spec_accept        batched acceptance + residual / bonus resampling (or greedy)
  *   md_philox_u32         counter-based uniforms feeding md_spec_accept
@@ -153,6 +154,28 @@ MD_API md_status md_verify_attn_full(const md_kv_cache* cache, const void* q, in
 MD_API md_status md_draft_attn_sparse(const md_kv_cache* cache, const void* q, int32_t num_q_heads, const int32_t* kv_len,
                                int32_t sink, int32_t window, float scale, float* out, float* lse, void* workspace,
                                size_t workspace_bytes, md_stream_t stream);
+
+/*
+ * md_draft_attn_indexed — self-speculative draft attention over a static SnapKV-selected KV
+ * (the paper's best drafter; SnapKV with observation
+ * window 32 and average pooling 5; per-sequence budgets).
+ * For b < B, h < Hq, with n = kv_len[b], kv head u = h / g:
+ *     J = {idx[b][u][i] : i < idx_count[b]}  U  {tail_start[b] <= j < n}
+ *     out[b][h][:] = softmax_j(scale * q[b][h] . k[b][u][j]) @ v[b][u][J],  lse likewise.
+ * The listed rows are gathered from the shared cache in place (TMA tile::gather4), the tail
+ * (the observation window plus every token generated since prefill) is streamed.
+ *   idx: device int32 [B][Hkv][idx_stride], 16-byte aligned, idx_stride % 4 == 0; entries
+ *        0 <= idx < tail_start[b] (ascending order recommended for locality).
+ *   idx_count, tail_start: device int32 [B], idx_count[b] <= idx_stride.
+ *   q, out, lse, workspace: as md_draft_attn_sparse (workspace sized with T = 1).
+ * Supported: head_dim in {64, 128}, g <= 8, cache strides multiples of head_dim.
+ * Preconditions (device): tail_start[b] <= kv_len[b] <= capacity, idx_count[b] +
+ * kv_len[b] - tail_start[b] >= 1.
+ */
+MD_API md_status md_draft_attn_indexed(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                       const int32_t* kv_len, const int32_t* idx, int32_t idx_stride,
+                                       const int32_t* idx_count, const int32_t* tail_start, float scale, float* out,
+                                       float* lse, void* workspace, size_t workspace_bytes, md_stream_t stream);
 
 /*
  * md_philox_u32 — Philox4x32-10 uniforms for md_spec_accept (

@@ -7,7 +7,7 @@ tensor raises.
 
 Functions mirror the C calls (same names without the `md_` prefix):
     kv_append, attn_workspace_bytes, verify_attn_full, draft_attn_sparse,
-    philox_u32, spec_accept
+    draft_attn_indexed, philox_u32, spec_accept
 """
 from __future__ import annotations
 
@@ -24,7 +24,8 @@ MD_ACCEPT_SAMPLE, MD_ACCEPT_GREEDY = 0, 1
 
 # the symbols include/magicdec_b200.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_workspace_bytes",
-               "md_verify_attn_full", "md_draft_attn_sparse", "md_philox_u32", "md_spec_accept")
+               "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed", "md_philox_u32",
+               "md_spec_accept")
 
 
 class MDError(RuntimeError):
@@ -65,10 +66,13 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                         c_void_p, sz, c_void_p]
     lib.md_draft_attn_sparse.argtypes = [pc, c_void_p, i32, c_void_p, i32, i32, f32, c_void_p, c_void_p,
                                          c_void_p, sz, c_void_p]
+    lib.md_draft_attn_indexed.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, i32, c_void_p, c_void_p, f32,
+                                          c_void_p, c_void_p, c_void_p, sz, c_void_p]
     lib.md_philox_u32.argtypes = [u64, u64, i32, i32, c_void_p, c_void_p]
     lib.md_spec_accept.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, i32, i32, i32, ctypes.c_int,
                                    c_void_p, c_void_p, c_void_p, c_void_p]
-    for name in ("md_kv_append", "md_verify_attn_full", "md_draft_attn_sparse", "md_philox_u32", "md_spec_accept"):
+    for name in ("md_kv_append", "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed",
+                 "md_philox_u32", "md_spec_accept"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -141,6 +145,18 @@ def draft_attn_sparse(q, k_cache, v_cache, kv_len, sink, window, scale, out, lse
     ws, wsb = _ws(workspace)
     _check(lib.md_draft_attn_sparse(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(kv_len), int(sink), int(window),
                                     float(scale), _ptr(out), _ptr(lse), ws, wsb, _stream(stream)))
+
+
+def draft_attn_indexed(q, k_cache, v_cache, kv_len, idx, idx_count, tail_start, scale, out, lse=None,
+                       workspace=None, stream=None):
+    """SnapKV draft: q [B, Hq, d] over idx[b, u, :idx_count[b]] U [tail_start[b], kv_len[b]).
+    idx is int32 [B, Hkv, K] (K % 4 == 0)."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_draft_attn_indexed(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(kv_len), _ptr(idx), idx.shape[2],
+                                     _ptr(idx_count), _ptr(tail_start), float(scale), _ptr(out), _ptr(lse), ws, wsb,
+                                     _stream(stream)))
 
 
 def philox_u32(seed, step, out, stream=None):

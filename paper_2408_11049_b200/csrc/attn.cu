@@ -43,11 +43,12 @@ constexpr int BOX_ROWS = 16;  // rows per TMA box of a partial tile (fetch granu
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
-enum : int { MODE_VERIFY = 0, MODE_DRAFT = 1 };
+enum : int { MODE_VERIFY = 0, MODE_DRAFT = 1, MODE_INDEXED = 2 };
 
-// K and V tensor maps with a full-tile box (TK rows) and a partial-tile box (BOX_ROWS rows).
+// K and V tensor maps with a full-tile box (TK rows) and a partial-tile box (BOX_ROWS rows);
+// for the index-list draft also 2-D row views of K and V for tile::gather4.
 struct TmapSet {
-  CUtensorMap k_full, v_full, k_part, v_part;
+  CUtensorMap k_full, v_full, k_part, v_part, k_rows, v_rows;
 };
 
 struct AttnParams {
@@ -59,19 +60,25 @@ struct AttnParams {
   int* counters;          // [B*Hkv] arrival counters (zero between calls)
   const int32_t* kv_len;  // [B]
   int B, Hq, Hkv, T, g, R;
-  int sink, window;       // draft only
+  int sink, window;       // StreamingLLM draft only
+  const int32_t* idx;     // SnapKV draft: [B][Hkv][idx_stride] selected prefix positions (ascending)
+  const int32_t* idx_count;   // [B] selected positions per (b, kv head)
+  const int32_t* tail_start;  // [B] first position of the always-attended tail
+  int idx_stride;
+  int64_t row_sB, row_sH, row_sS;  // cache strides in units of rows (d elements), for gather4
   int mode;
   float scale_log2;       // scale * log2(e)
 };
 
 // ------------------------------------------------------------------ stream-K decomposition
-__device__ __forceinline__ int unit_keys(const AttnParams& p, int n) {
+__device__ __forceinline__ int unit_keys(const AttnParams& p, int n, int b) {
   if (p.mode == MODE_VERIFY) return n;
+  if (p.mode == MODE_INDEXED) return __ldg(p.idx_count + b) + max(0, n - __ldg(p.tail_start + b));
   const int nA = min(p.sink, n);
   return nA + max(0, n - max(p.sink, n - p.window));
 }
 __device__ __forceinline__ int unit_tiles(const AttnParams& p, int b) {
-  return (unit_keys(p, __ldg(p.kv_len + b)) + TK - 1) / TK;
+  return (unit_keys(p, __ldg(p.kv_len + b), b) + TK - 1) / TK;
 }
 // Per-CTA prefix table over sequences in shared memory: pre[b] = sum_{b' < b} Hkv * tiles(b')
 // (built once per CTA with one parallel load of kv_len, so locating a CTA's range costs a
@@ -187,16 +194,23 @@ struct SegWalker {
   }
 };
 
-// Physical key ranges [s0, e0) then [s1, e1) of the segment's logical keys.
+// Key ranges [s0, e0) then [s1, e1) of the segment's logical keys.  Part 1 is always a range
+// of cache rows; part 0 is a range of cache rows too, except in MODE_INDEXED where it is a
+// range of positions in the unit's index list (gathered row by row).
 struct Ranges {
   int s0, e0, s1, e1;
 };
 __device__ __forceinline__ Ranges seg_ranges(const AttnParams& p, const Seg& sg) {
-  const int keys = unit_keys(p, sg.n);
+  const int keys = unit_keys(p, sg.n, sg.b);
   const int lo = sg.lo * TK, hi = min(keys, sg.hi * TK);
   Ranges r{lo, lo, 0, 0};
   if (p.mode == MODE_VERIFY) {
     r.e0 = max(lo, hi);
+  } else if (p.mode == MODE_INDEXED) {
+    const int cnt = __ldg(p.idx_count + sg.b), tail = __ldg(p.tail_start + sg.b);
+    r.e0 = max(lo, min(hi, cnt));                  // index-list entries
+    r.s1 = tail + (max(lo, cnt) - cnt);            // tail rows
+    r.e1 = max(r.s1, tail + (hi - cnt));
   } else {
     const int nA = min(p.sink, sg.n);
     const int startB = max(p.sink, sg.n - p.window);
@@ -218,20 +232,51 @@ __device__ __forceinline__ int64_t out_row(const AttnParams& p, int b, int kvh, 
 
 // ------------------------------------------------------------------ producer
 // Stream the K/V tiles of one segment into the ring; `it` is the running tile counter.
+// Called by all 32 lanes of the producer warp (lane 0 owns the barriers; in MODE_INDEXED
+// lanes 0..15 each gather 4 listed rows of an index-list tile with tile::gather4).
 template <int D, int NSTAGE>
-__device__ __forceinline__ void produce_segment(const TmapSet& tm, const Ranges& rg, int b, int kvh, uint8_t* ring,
-                                                uint64_t* full, uint64_t* empty, int& it, uint64_t pol) {
+__device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapSet& tm, const Ranges& rg, int b,
+                                                int kvh, uint8_t* ring, uint64_t* full, uint64_t* empty, int& it,
+                                                uint64_t pol) {
   constexpr int SUB = D / 64, TILE = TK * D * 2, STAGE = 2 * TILE;
+  const int lane = threadIdx.x & 31;
+  const bool gathered0 = (p.mode == MODE_INDEXED);
 #pragma unroll 1
   for (int part = 0; part < 2; ++part) {
     const int rs = part ? rg.s1 : rg.s0, re = part ? rg.e1 : rg.e0;
 #pragma unroll 1
     for (int pos = rs; pos < re; pos += TK, ++it) {
       const int stage = it % NSTAGE;
-      mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
       const int nvalid = min(TK, re - pos);
       uint8_t* kt = ring + stage * STAGE;
       uint8_t* vt = kt + TILE;
+      if (part == 0 && gathered0) {
+        // rows idx[b][kvh][pos .. pos + nvalid), 4 per gather4; padding rows repeat a valid row
+        const int ngrp = (nvalid + 3) / 4;
+        if (lane == 0) {
+          mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[stage], ngrp * 4 * 128 * SUB * 2);
+        }
+        __syncwarp();
+        if (lane < ngrp) {
+          const int32_t* ip = p.idx + ((int64_t)b * p.Hkv + kvh) * p.idx_stride + pos;
+          int row[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = min(4 * lane + u, nvalid - 1);
+            row[u] = static_cast<int>(b * p.row_sB + kvh * p.row_sH + (int64_t)__ldg(ip + e) * p.row_sS);
+          }
+          for (int sub = 0; sub < SUB; ++sub) {
+            const int off = sub * TK * 128 + lane * 4 * 128;
+            tma_gather4(kt + off, &tm.k_rows, &full[stage], sub * 64, row[0], row[1], row[2], row[3], pol);
+            tma_gather4(vt + off, &tm.v_rows, &full[stage], sub * 64, row[0], row[1], row[2], row[3], pol);
+          }
+        }
+        __syncwarp();
+        continue;
+      }
+      if (lane != 0) continue;
+      mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
       if (nvalid == TK) {  // full tile: one TK-row box per 128-byte column slab
         mbar_arrive_expect_tx(&full[stage], STAGE);
         for (int sub = 0; sub < SUB; ++sub) {
@@ -360,19 +405,26 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
   Seg sg;
 
   if (warp == NC) {
-    // ============================== TMA producer ==============================
+    // ============================== TMA producer warp ==============================
     if (lane == 0) {
       prefetch_tmap(&tm.k_full);
       prefetch_tmap(&tm.v_full);
       prefetch_tmap(&tm.k_part);
       prefetch_tmap(&tm.v_part);
-      const uint64_t pol = policy_evict_first();
-      int it = 0, si = 0;
-      while (walk.next(p, sg)) {
-        if (si > 0) mbar_wait(epi_done, (si - 1) & 1);  // the ring doubles as epilogue scratch
-        produce_segment<D, NSTAGE>(tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol);
-        ++si;
+      if (p.mode == MODE_INDEXED) {
+        prefetch_tmap(&tm.k_rows);
+        prefetch_tmap(&tm.v_rows);
       }
+    }
+    const uint64_t pol = policy_evict_first();
+    int it = 0, si = 0;
+    while (walk.next(p, sg)) {
+      if (si > 0) {  // the ring doubles as epilogue scratch
+        if (lane == 0) mbar_wait(epi_done, (si - 1) & 1);
+        __syncwarp();
+      }
+      produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol);
+      ++si;
     }
     return;
   }
@@ -678,24 +730,31 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   Seg sg;
 
   if (warp == NC) {
-    // ============================== producer (one lane) ==============================
+    // ============================== TMA producer warp ==============================
     if (lane == 0) {
       prefetch_tmap(&tm.k_full);
       prefetch_tmap(&tm.v_full);
       prefetch_tmap(&tm.k_part);
       prefetch_tmap(&tm.v_part);
-      const uint64_t pol = policy_evict_first();
-      int it = 0, qi = 0;
-      while (walk.next(p, sg)) {
-        // this segment's query rows: row r = (t = r / g, head = kvh*g + r % g)
+      if (p.mode == MODE_INDEXED) {
+        prefetch_tmap(&tm.k_rows);
+        prefetch_tmap(&tm.v_rows);
+      }
+    }
+    const uint64_t pol = policy_evict_first();
+    int it = 0, qi = 0;
+    while (walk.next(p, sg)) {
+      // this segment's query rows: row r = (t = r / g, head = kvh*g + r % g)
+      if (lane == 0) {
         const int qs = qi & 1;
         mbar_wait(&qempty[qs], ((qi >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&qfull[qs], p.R * D * 2);
         for (int r = 0; r < p.R; ++r)
           bulk_load(qbuf + (qs * C::ROWS + r) * C::QSTR, p.q + out_row(p, sg.b, sg.kvh, r) * D, D * 2, &qfull[qs]);
-        produce_segment<D, NSTAGE>(tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol);
-        ++qi;
       }
+      __syncwarp();
+      produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol);
+      ++qi;
     }
     return;
   }
@@ -960,6 +1019,25 @@ static md_status make_tmap(CUtensorMap* m, const md_kv_cache* c, void* base, int
   return MD_OK;
 }
 
+// 2-D view of a cache as rows of d elements (row = b*row_sB + h*row_sH + pos*row_sS), box
+// {64 columns, 1 row} with SWIZZLE_128B, for tile::gather4 of listed rows.
+static md_status make_row_tmap(CUtensorMap* m, const md_kv_cache* c, void* base) {
+  auto enc = get_encode();
+  MD_REQUIRE(enc != nullptr, MD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  const int64_t d = c->head_dim;
+  const int64_t rows = (c->batch - 1) * (c->stride_b / d) + (c->num_kv_heads - 1) * (c->stride_h / d) +
+                       (c->capacity - 1) * (c->stride_s / d) + 1;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MD_REQUIRE(r == CUDA_SUCCESS, MD_ERR_INVALID_ARG, "cuTensorMapEncodeTiled (row view) failed (code %d)", (int)r);
+  return MD_OK;
+}
+
 template <typename K>
 static md_status set_smem(K kern, int bytes, int* done_dev) {
   int dev = 0;
@@ -1018,9 +1096,16 @@ static md_status check_cache(const md_kv_cache* c, const char* who) {
   return MD_OK;
 }
 
+struct IndexedArgs {
+  const int32_t* idx = nullptr;
+  int idx_stride = 0;
+  const int32_t* idx_count = nullptr;
+  const int32_t* tail_start = nullptr;
+};
+
 static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int T, const int32_t* kv_len, int sink,
                                int window, int mode, float scale, float* out, float* lse, void* ws, size_t ws_bytes,
-                               cudaStream_t s, const char* who) {
+                               cudaStream_t s, const char* who, const IndexedArgs& ix = IndexedArgs()) {
   md_status st = check_cache(c, who);
   if (st != MD_OK) return st;
   MD_REQUIRE(q != nullptr && kv_len != nullptr && out != nullptr, MD_ERR_INVALID_ARG, "%s: NULL q/kv_len/out", who);
@@ -1040,6 +1125,16 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
       (st = make_tmap(&tm.k_part, c, c->k, BOX_ROWS)) != MD_OK ||
       (st = make_tmap(&tm.v_part, c, c->v, BOX_ROWS)) != MD_OK)
     return st;
+  if (mode == MODE_INDEXED) {
+    MD_REQUIRE(R <= 8, MD_ERR_UNSUPPORTED, "%s: at most 8 query heads per KV head", who);
+    MD_REQUIRE(c->stride_s % c->head_dim == 0 && c->stride_h % c->head_dim == 0 && c->stride_b % c->head_dim == 0,
+               MD_ERR_UNSUPPORTED, "%s: cache strides must be multiples of head_dim for row gathers", who);
+    if ((st = make_row_tmap(&tm.k_rows, c, c->k)) != MD_OK || (st = make_row_tmap(&tm.v_rows, c, c->v)) != MD_OK)
+      return st;
+  } else {
+    tm.k_rows = tm.k_full;  // unused
+    tm.v_rows = tm.v_full;
+  }
   AttnParams p{};
   p.q = static_cast<const uint16_t*>(q);
   p.out = out;
@@ -1055,6 +1150,13 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.window = window;
   p.mode = mode;
   p.scale_log2 = scale * LOG2E;
+  p.idx = ix.idx;
+  p.idx_stride = ix.idx_stride;
+  p.idx_count = ix.idx_count;
+  p.tail_start = ix.tail_start;
+  p.row_sB = c->stride_b / c->head_dim;
+  p.row_sH = c->stride_h / c->head_dim;
+  p.row_sS = c->stride_s / c->head_dim;
   uint8_t* w = static_cast<uint8_t*>(ws);
   p.ws_o = reinterpret_cast<float*>(w);
   w += align256((size_t)grid * 2 * R * c->head_dim * 4);
@@ -1100,4 +1202,25 @@ extern "C" md_status md_draft_attn_sparse(const md_kv_cache* cache, const void* 
              "md_draft_attn_sparse: need sink >= 0, window >= 0, sink + window >= 1");
   return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, out, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse");
+}
+
+extern "C" md_status md_draft_attn_indexed(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                           const int32_t* kv_len, const int32_t* idx, int32_t idx_stride,
+                                           const int32_t* idx_count, const int32_t* tail_start, float scale,
+                                           float* out, float* lse, void* workspace, size_t workspace_bytes,
+                                           md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(cache != nullptr, MD_ERR_INVALID_ARG, "md_draft_attn_indexed: NULL cache");
+  MD_REQUIRE(idx != nullptr && idx_count != nullptr && tail_start != nullptr, MD_ERR_INVALID_ARG,
+             "md_draft_attn_indexed: NULL idx / idx_count / tail_start");
+  MD_REQUIRE(idx_stride >= 0 && idx_stride % 4 == 0 && aligned16(idx), MD_ERR_INVALID_ARG,
+             "md_draft_attn_indexed: idx must be 16-byte aligned with idx_stride a multiple of 4");
+  IndexedArgs ix;
+  ix.idx = idx;
+  ix.idx_stride = idx_stride;
+  ix.idx_count = idx_count;
+  ix.tail_start = tail_start;
+  return run_attention(cache, q, num_q_heads, 1, kv_len, 0, 0, MODE_INDEXED, scale, out, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_draft_attn_indexed", ix);
 }
