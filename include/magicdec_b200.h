@@ -14,6 +14,7 @@
  *   md_kv_append          write the new K/V rows of a pass into the shared cache
  *   md_draft_attn_sparse  1 query token / sequence over sink ∪ window (no KV copy)
  *   md_draft_attn_indexed 1 query token / sequence over a SnapKV index list ∪ recent tail
+ *   md_snapkv_select      prefill-time SnapKV selection of that index list
  *   md_verify_attn_full   gamma+1 query tokens / sequence over the full KV, GQA, causal
  *   md_spec_accept        batched acceptance + residual / bonus resampling (or greedy)
  *   md_philox_u32         counter-based uniforms feeding md_spec_accept
@@ -176,6 +177,34 @@ MD_API md_status md_draft_attn_indexed(const md_kv_cache* cache, const void* q, 
                                        const int32_t* kv_len, const int32_t* idx, int32_t idx_stride,
                                        const int32_t* idx_count, const int32_t* tail_start, float scale, float* out,
                                        float* lse, void* workspace, size_t workspace_bytes, md_stream_t stream);
+
+/*
+ * md_snapkv_select — SnapKV static KV selection at prefill for md_draft_attn_indexed
+ * (P:1141 footnote: observation window 32, average pooling kernel 5;
+ * a static method, so drafting pays no per-step selection cost, Eq.3).  Per
+ * sequence b (prompt length L = prefill_len[b]) and KV head u, with the g*w window queries
+ * q_obs[b][i][u*g + hh] (prompt positions L-w+i):
+ *   S1 a[hh,i,j] = softmax_j(scale q . k[b][u][j]) over the causal keys j <= L-w+i;
+ *   S2 vote[j]   = sum_{hh,i} a[hh,i,j]                 for j < L-w;
+ *   S3 pooled[j] = (vote[j-2] + ... + vote[j+2]) / 5     (zero padding);
+ *   S4 idx[b][u][0 .. c) = the c = min(budget-w, L-w) largest pooled positions (ties ->
+ *      lower position), ascending; idx_count[b] = c.  Entries past c are left untouched.
+ * The draft then attends to idx U [L-w, n) (pass tail_start = L - w).  Scores are fp32 on
+ * the tensor cores, so positions whose pooled votes tie to ~1e-6 relative may order
+ * differently from an fp64 evaluation.
+ *   q_obs: device bf16 [B][w][Hq][head_dim]; prefill_len: device int32[B];
+ *   max_prefill_len: host bound >= every prefill_len[b];
+ *   idx: device int32 [B][Hkv][idx_stride] (idx_stride >= budget - w); idx_count: int32[B];
+ *   workspace: >= md_snapkv_workspace_bytes(B, Hq, Hkv, w, max_prefill_len) bytes (no init).
+ * Supported: head_dim in {64, 128}, g*w <= 256.
+ * Preconditions (device): w <= prefill_len[b] <= max_prefill_len.
+ */
+MD_API size_t md_snapkv_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads, int32_t w,
+                                        int32_t max_prefill_len);
+MD_API md_status md_snapkv_select(const md_kv_cache* cache, const void* q_obs, int32_t num_q_heads,
+                                  const int32_t* prefill_len, int32_t max_prefill_len, int32_t w, int32_t budget,
+                                  float scale, int32_t* idx, int32_t idx_stride, int32_t* idx_count, void* workspace,
+                                  size_t workspace_bytes, md_stream_t stream);
 
 /*
  * md_philox_u32 — Philox4x32-10 uniforms for md_spec_accept (

@@ -7,7 +7,7 @@ tensor raises.
 
 Functions mirror the C calls (same names without the `md_` prefix):
     kv_append, attn_workspace_bytes, verify_attn_full, draft_attn_sparse,
-    draft_attn_indexed, philox_u32, spec_accept
+    draft_attn_indexed, snapkv_workspace_bytes, snapkv_select, philox_u32, spec_accept
 """
 from __future__ import annotations
 
@@ -24,8 +24,8 @@ MD_ACCEPT_SAMPLE, MD_ACCEPT_GREEDY = 0, 1
 
 # the symbols include/magicdec_b200.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_workspace_bytes",
-               "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed", "md_philox_u32",
-               "md_spec_accept")
+               "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed", "md_snapkv_workspace_bytes",
+               "md_snapkv_select", "md_philox_u32", "md_spec_accept")
 
 
 class MDError(RuntimeError):
@@ -68,11 +68,15 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                          c_void_p, sz, c_void_p]
     lib.md_draft_attn_indexed.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, i32, c_void_p, c_void_p, f32,
                                           c_void_p, c_void_p, c_void_p, sz, c_void_p]
+    lib.md_snapkv_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
+    lib.md_snapkv_workspace_bytes.restype = sz
+    lib.md_snapkv_select.argtypes = [pc, c_void_p, i32, c_void_p, i32, i32, i32, f32, c_void_p, i32, c_void_p,
+                                     c_void_p, sz, c_void_p]
     lib.md_philox_u32.argtypes = [u64, u64, i32, i32, c_void_p, c_void_p]
     lib.md_spec_accept.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, i32, i32, i32, ctypes.c_int,
                                    c_void_p, c_void_p, c_void_p, c_void_p]
     for name in ("md_kv_append", "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed",
-                 "md_philox_u32", "md_spec_accept"):
+                 "md_snapkv_select", "md_philox_u32", "md_spec_accept"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -157,6 +161,25 @@ def draft_attn_indexed(q, k_cache, v_cache, kv_len, idx, idx_count, tail_start, 
     _check(lib.md_draft_attn_indexed(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(kv_len), _ptr(idx), idx.shape[2],
                                      _ptr(idx_count), _ptr(tail_start), float(scale), _ptr(out), _ptr(lse), ws, wsb,
                                      _stream(stream)))
+
+
+def snapkv_workspace_bytes(batch, num_q_heads, num_kv_heads, w, max_prefill_len) -> int:
+    return int(load_library().md_snapkv_workspace_bytes(batch, num_q_heads, num_kv_heads, w, max_prefill_len))
+
+
+def snapkv_select(k_cache, v_cache, q_obs, prefill_len, max_prefill_len, w, budget, scale, idx, idx_count,
+                  workspace=None, stream=None):
+    """SnapKV selection at prefill: q_obs [B, w, Hq, d] bf16 -> idx [B, Hkv, K] int32 (ascending
+    positions, K >= budget - w), idx_count [B] int32."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    if workspace is None:
+        workspace = torch.empty(snapkv_workspace_bytes(q_obs.shape[0], q_obs.shape[2], k_cache.shape[1], w,
+                                                       max_prefill_len), dtype=torch.uint8, device=q_obs.device)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_snapkv_select(ctypes.byref(c), _ptr(q_obs), q_obs.shape[2], _ptr(prefill_len), int(max_prefill_len),
+                                int(w), int(budget), float(scale), _ptr(idx), idx.shape[2], _ptr(idx_count), ws, wsb,
+                                _stream(stream)))
 
 
 def philox_u32(seed, step, out, stream=None):

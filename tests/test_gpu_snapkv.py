@@ -81,3 +81,49 @@ def test_indexed_equals_streaming_draft_on_gpu():
     md.draft_attn_sparse(case.qd, case.k, case.v, case.kv_len_t, sink, window, case.scale, out, lse, ws)
     torch.cuda.synchronize()
     assert np.array_equal(o, out.cpu().numpy()) and np.array_equal(l, lse.cpu().numpy())
+
+
+def _check_selection(idx_gpu, cnt_gpu, idx_ref, cnt_ref, pooled_ref, rel_tol=1e-4):
+    """Same count; the selected sets are identical except for positions whose fp64 pooled
+    scores tie the selection threshold within rel_tol (fp32 vs fp64 order near ties)."""
+    assert np.array_equal(cnt_gpu, cnt_ref)
+    B, Hkv = idx_ref.shape[:2]
+    ndiff = 0
+    for b in range(B):
+        c = int(cnt_ref[b])
+        for h in range(Hkv):
+            g = idx_gpu[b, h, :c]
+            r = idx_ref[b, h, :c]
+            assert np.all(np.diff(g) > 0), "GPU selection must be strictly ascending"
+            pooled = pooled_ref[b][h]
+            if c == len(pooled):
+                assert np.array_equal(g, r)
+                continue
+            thr = np.sort(pooled)[::-1][c - 1]
+            diff = set(g.tolist()) ^ set(r.tolist())
+            ndiff += len(diff)
+            for x in diff:
+                assert abs(pooled[x] - thr) <= rel_tol * pooled.max(), (b, h, x, pooled[x], thr)
+    return ndiff
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,L,w,budget,regime", [
+    (2, 8, 2, 128, [3000, 2100], 32, 256, "peaky"),
+    (3, 32, 8, 128, [1500, 1400, 700], 32, 512, "flat"),
+    (2, 28, 4, 128, [2500, 300], 32, 1024, "peaky"),          # short prompt: keep everything
+    (2, 4, 4, 64, [900, 1000], 8, 100, "peaky"),
+])
+def test_snapkv_select_matches_oracle(B, Hq, Hkv, d, L, w, budget, regime):
+    import synth as S
+    reg = S.Regime(regime, sink=4, needle_period=97) if regime == "peaky" else S.FLAT
+    cap = max(L) + 8
+    case = AttnCase(B, Hq, Hkv, d, cap, L, seed=B * 100 + Hq, regime=reg).to_cuda()
+    q_obs_bits = k_to_bf16_bits(S.q_rows_k(B + 5, S.T_QVERIFY, B, w, Hq, Hkv, d, regime=reg))
+    stride = ((budget - w) + 3) // 4 * 4
+    idx = torch.full((B, Hkv, stride), -1, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(B, dtype=torch.int32, device="cuda")
+    md.snapkv_select(case.k, case.v, bits_to_torch_bf16(q_obs_bits), torch.tensor(L, dtype=torch.int32).cuda(),
+                     max(L), w, budget, case.scale, idx, cnt)
+    torch.cuda.synchronize()
+    ref_idx, ref_cnt, pooled = SK.snapkv_select(q_obs_bits, case.k_bits, np.array(L), w, budget, case.scale)
+    _check_selection(idx.cpu().numpy(), cnt.cpu().numpy(), ref_idx, ref_cnt, pooled)

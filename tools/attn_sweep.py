@@ -41,8 +41,7 @@ def sweep(cfg, R=3, reps=12):
     out_d = torch.empty((B, Hq, d), device="cuda")
     lse_d = torch.empty((B, Hq), device="cuda")
     ws_v = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, T, mkl)), dtype=torch.uint8, device="cuda")
-    ws_d = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, sink + window)), dtype=torch.uint8,
-                       device="cuda")
+    ws_d = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, cap)), dtype=torch.uint8, device="cuda")
 
     def t(fn):
         fn(0)
@@ -57,10 +56,24 @@ def sweep(cfg, R=3, reps=12):
 
     vms = t(lambda i: md.verify_attn_full(qv, kc[i % R], vc[i % R], kvv, mkl, scale, out_v, lse_v, ws_v))
     dms = t(lambda i: md.draft_attn_sparse(qd, kc[i % R], vc[i % R], kvd, sink, window, scale, out_d, lse_d, ws_d))
+    # SnapKV draft: 2048-token budget = 2016 listed prefix rows + the 32-token window tail
+    w_obs, budget = 32, 2048
+    rng = np.random.default_rng(0)
+    idx = np.zeros((B, Hkv, budget - w_obs), np.int32)
+    for b in range(B):
+        for h in range(Hkv):
+            idx[b, h] = np.sort(rng.choice(int(L0[b]) - w_obs, size=budget - w_obs, replace=False))
+    idx_t = torch.from_numpy(idx).cuda()
+    cnt_t = torch.full((B,), budget - w_obs, dtype=torch.int32, device="cuda")
+    tail_t = torch.from_numpy((L0 - w_obs).astype(np.int32)).cuda()
+    sms = t(lambda i: md.draft_attn_indexed(qd, kc[i % R], vc[i % R], kvd, idx_t, cnt_t, tail_t, scale, out_d, lse_d,
+                                            ws_d))
+    sb = int(B * Hkv * (budget + 1) * d * 4 + B * Hq * d * 6 + B * Hq * 4)
     vb = verify_bytes(L0 + T, Hkv, Hq, d, T)
     db = draft_bytes(L0 + 1, Hkv, Hq, d, sink, window)
     res = {"cfg": cfg, "verify_ms": round(vms, 4), "verify_gbs": round(vb / vms / 1e6, 1),
            "draft_us": round(dms * 1e3, 2), "draft_gbs": round(db / dms / 1e6, 1),
+           "snapkv_draft_us": round(sms * 1e3, 2), "snapkv_draft_gbs": round(sb / sms / 1e6, 1),
            "env": {k: v for k, v in os.environ.items() if k.startswith("MD_")}}
     print(json.dumps(res), flush=True)
     del kc, vc
