@@ -244,6 +244,14 @@ MD_API md_status md_spec_accept(const float* p, const float* q, const int32_t* d
                          int32_t B, int32_t gamma, int32_t V, md_accept_mode mode, int32_t* out_tokens,
                          int32_t* num_accepted, int32_t* committed_len_inout, md_stream_t stream);
 
+/*
+ * md_debug_trace — diagnostics only.  While `buf` (device uint64 [G][8], G = CTAs of the
+ * attention grid; 0 disables) is set, every attention call stamps %globaltimer per CTA at:
+ * entry, after the grid-dependency wait, after locating its stream-K range, first K/V tile
+ * landed, last segment epilogue start, end.  Process-wide, not thread-safe; NULL disables.
+ */
+MD_API md_status md_debug_trace(void* buf, size_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,7 +25,7 @@ MD_ACCEPT_SAMPLE, MD_ACCEPT_GREEDY = 0, 1
 # the symbols include/magicdec_b200.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_workspace_bytes",
                "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed", "md_snapkv_workspace_bytes",
-               "md_snapkv_select", "md_philox_u32", "md_spec_accept")
+               "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace")
 
 
 class MDError(RuntimeError):
@@ -75,8 +75,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.md_philox_u32.argtypes = [u64, u64, i32, i32, c_void_p, c_void_p]
     lib.md_spec_accept.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, i32, i32, i32, ctypes.c_int,
                                    c_void_p, c_void_p, c_void_p, c_void_p]
+    lib.md_debug_trace.argtypes = [c_void_p, sz]
     for name in ("md_kv_append", "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed",
-                 "md_snapkv_select", "md_philox_u32", "md_spec_accept"):
+                 "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -198,3 +199,9 @@ def spec_accept(p, q, draft_tokens, rnd, out_tokens, num_accepted, committed_len
     m = MD_ACCEPT_SAMPLE if mode == "sample" else MD_ACCEPT_GREEDY
     _check(lib.md_spec_accept(_ptr(p), _ptr(q), _ptr(draft_tokens), _ptr(rnd), B, G1 - 1, V, m, _ptr(out_tokens),
                               _ptr(num_accepted), _ptr(committed_len), _stream(stream)))
+
+
+def debug_trace(buf=None):
+    """Diagnostics: stamp per-CTA phase times of every attention call into buf (int64 [G, 8])."""
+    lib = load_library()
+    _check(lib.md_debug_trace(_ptr(buf), 0 if buf is None else buf.numel() * 8))

@@ -1,4 +1,6 @@
 // abi.cu — library-wide ABI entry points: version, thread-local error string, device query.
+#include <cstdlib>
+
 #include "md_internal.h"
 
 namespace md {
@@ -15,6 +17,14 @@ void set_error(const char* fmt, ...) {
 }
 
 void clear_error() { g_last_error.clear(); }
+
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("MD_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
 
 int device_sm_count() {
   int dev = 0, n = 0;

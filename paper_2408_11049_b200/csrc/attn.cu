@@ -66,6 +66,7 @@ struct AttnParams {
   const int32_t* tail_start;  // [B] first position of the always-attended tail
   int idx_stride;
   int64_t row_sB, row_sH, row_sS;  // cache strides in units of rows (d elements), for gather4
+  unsigned long long* trace;       // diagnostics: [G][8] globaltimer stamps (md_debug_trace), or null
   int mode;
   float scale_log2;       // scale * log2(e)
 };
@@ -82,9 +83,9 @@ __device__ __forceinline__ int unit_tiles(const AttnParams& p, int b) {
 }
 // Per-CTA prefix table over sequences in shared memory: pre[b] = sum_{b' < b} Hkv * tiles(b')
 // (built once per CTA with one parallel load of kv_len, so locating a CTA's range costs a
-// binary search instead of B dependent global loads).  Batches larger than TABLE_B fall
-// back to walking kv_len in global memory.
-constexpr int TABLE_B = 1024;
+// binary search instead of B dependent global loads).  Batches larger than TABLE_B (256)
+// fall back to walking kv_len in global memory.
+constexpr int TABLE_B = 256;
 constexpr int TABLE_BYTES = (TABLE_B + 1) * 4 + 60;
 
 __device__ void build_prefix(const AttnParams& p, int* pre) {
@@ -224,6 +225,11 @@ __device__ __forceinline__ Ranges seg_ranges(const AttnParams& p, const Seg& sg)
 // The partial slot of CTA c for a unit starting at ustart: 0 if it is c's first unit, 1 if its last.
 __device__ __forceinline__ int slot_of(int64_t ustart, int c, int64_t total, int G) {
   return ustart > cta_start(c, total, G) ? 1 : 0;
+}
+
+// diagnostics: consumer warp 0 / lane 0 stamps phase k of this CTA (md_debug_trace)
+__device__ __forceinline__ void trace_stamp(const AttnParams& p, int k) {
+  if (p.trace != nullptr && threadIdx.x == 0) p.trace[blockIdx.x * 8 + k] = globaltimer();
 }
 
 __device__ __forceinline__ int64_t out_row(const AttnParams& p, int b, int kvh, int r) {
@@ -394,6 +400,10 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
     mbar_init(epi_done, NC);
     fence_mbar_init();
   }
+  trace_stamp(p, 0);
+  pdl_trigger();
+  pdl_wait();  // kv_len, the cache and q may come from the previous kernel
+  trace_stamp(p, 1);
   __syncthreads();
   build_prefix(p, pre);
   const int64_t total = total_tiles(p, pre);
@@ -403,6 +413,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
   SegWalker walk;
   walk.init(p, pre, S, E);
   Seg sg;
+  trace_stamp(p, 2);
 
   if (warp == NC) {
     // ============================== TMA producer warp ==============================
@@ -475,6 +486,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
       for (int pos = rs; pos < re; pos += TK, ++it) {
         const int stage = it % NSTAGE;
         mbar_wait(&full[stage], (it / NSTAGE) & 1);
+        if (it == 0) trace_stamp(p, 3);
         const int nvalid = min(TK, re - pos);
         const int kw0 = ks * KW;
         if (kw0 < nvalid) {
@@ -579,6 +591,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
     }
 
     // ============================== segment epilogue ==============================
+    trace_stamp(p, 4);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
@@ -652,6 +665,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
     fence_proxy_async();         // order our generic writes to the ring before later TMA writes
     named_bar_sync(1, NC * 32);  // the scratch (= ring) may now be refilled
     if (lane == 0) mbar_arrive(epi_done);
+    trace_stamp(p, 5);
   }
 }
 
@@ -672,8 +686,8 @@ struct KeysCfg {
   static constexpr int STAGE = 2 * TILE;
   static constexpr int QSTR = D * 2 + 16;  // padded smem row of Q (conflict-free ldmatrix)
   static constexpr int QBUF = 2 * ROWS * QSTR;
-  static constexpr int OSTR = ROWS + 1;    // fp32 epilogue stride per d (transposed O)
-  static constexpr int EPI = NC * D * OSTR * 4 + NC * ROWS * 2 * 4 + ROWS * 4 + 64;
+  static constexpr int FRAG = (D / 16) * 4 * 32;  // fp32 of one warp's O^T fragments
+  static constexpr int EPI = (NC / 2) * FRAG * 4 + NC * ROWS * 2 * 4 + ROWS * 4 + 64;
   static constexpr int FIXED = QBUF + EPI + 256 /*barriers*/ + TABLE_BYTES + 1024 /*alignment slack*/;
   static constexpr int NSTAGE_FIT = ((CTAS == 1 ? 227 * 1024 : 112 * 1024) - FIXED) / STAGE;
   static constexpr int NSTAGE = NSTAGE_FIT > 8 ? 8 : NSTAGE_FIT;
@@ -686,14 +700,15 @@ template <int D, int KS, int CTAS>
 __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     attn_keys_kernel(const __grid_constant__ TmapSet tm, const AttnParams p) {
   using C = KeysCfg<D, KS, CTAS>;
-  constexpr int NC = C::NC, KW = C::KW, KB = C::KB, NSTAGE = C::NSTAGE, OSTR = C::OSTR;
+  constexpr int NC = C::NC, KW = C::KW, KB = C::KB, NSTAGE = C::NSTAGE, FRAG = C::FRAG;
+  static_assert(NC == 4, "the epilogue tree merge assumes 4 consumer warps");
   constexpr int MD16 = D / 16;  // m16 tiles of O^T (head-dim rows) == k16 steps of S^T
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* qbuf = smem + NSTAGE * C::STAGE;
-  float* obuf = reinterpret_cast<float*>(qbuf + C::QBUF);  // [NC][D][OSTR]   O^T per warp
-  float* mlbuf = obuf + NC * D * OSTR;                      // [NC][8][2]      (m, l) per warp row
+  float* obuf = reinterpret_cast<float*>(qbuf + C::QBUF);  // [NC/2][FRAG]    O^T fragments (tree merge)
+  float* mlbuf = obuf + (NC / 2) * FRAG;                    // [NC][8][2]      (m, l) per warp row
   float* lsebuf = mlbuf + NC * C::ROWS * 2;                 // [8]             combined lse (log2)
   int* flag = reinterpret_cast<int*>(lsebuf + C::ROWS);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(obuf) + C::EPI);
@@ -719,6 +734,10 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     const int row = i / (D / 8), c = i - row * (D / 8);
     if ((row % C::ROWS) >= p.R) *reinterpret_cast<uint4*>(qbuf + row * C::QSTR + c * 16) = make_uint4(0, 0, 0, 0);
   }
+  trace_stamp(p, 0);
+  pdl_trigger();
+  pdl_wait();  // kv_len, the cache and q may come from the previous kernel
+  trace_stamp(p, 1);
   __syncthreads();
   build_prefix(p, pre);
   const int64_t total = total_tiles(p, pre);
@@ -728,6 +747,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   SegWalker walk;
   walk.init(p, pre, S, E);
   Seg sg;
+  trace_stamp(p, 2);
 
   if (warp == NC) {
     // ============================== TMA producer warp ==============================
@@ -800,6 +820,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       for (int pos = rs; pos < re; pos += TK, ++it) {
         const int stage = it % NSTAGE;
         mbar_wait(&full[stage], (it / NSTAGE) & 1);
+        if (it == 0) trace_stamp(p, 3);
         const int nvalid = min(TK, re - pos);
         const int kw0 = ks * KW;
         if (kw0 < nvalid) {
@@ -895,6 +916,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     }
 
     // ============================== segment epilogue ==============================
+    trace_stamp(p, 4);
     // full row sums: reduce over the 8 lanes sharing cq (they hold different keys)
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -928,38 +950,64 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         f[j] = (l[j] > 0.f) ? ex2(m[j] - M) / L : 0.f;
         if (ks == 0 && gq == 0) lsebuf[rl] = (L > 0.f) ? M + __log2f(L) : -INFINITY;
       }
-      float* ob = obuf + (size_t)warp * D * OSTR;
 #pragma unroll
       for (int i = 0; i < MD16; ++i) {
-        const int d0 = i * 16 + gq, r0 = 2 * cq;
-        ob[d0 * OSTR + r0] = o[i][0] * f[0];
-        ob[d0 * OSTR + r0 + 1] = o[i][1] * f[1];
-        ob[(d0 + 8) * OSTR + r0] = o[i][2] * f[0];
-        ob[(d0 + 8) * OSTR + r0 + 1] = o[i][3] * f[1];
+        o[i][0] *= f[0];
+        o[i][1] *= f[1];
+        o[i][2] *= f[0];
+        o[i][3] *= f[1];
       }
     }
+    // sum the KS = 4 slices in registers by a 2-round tree through shared memory (every warp
+    // holds the same fragment layout, so lane t adds lane t's values: conflict-free)
+    if (warp >= 2) {
+      float* ob = obuf + (warp - 2) * FRAG;
+#pragma unroll
+      for (int i = 0; i < MD16; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ob[(i * 4 + e) * 32 + lane] = o[i][e];
+    }
     named_bar_sync(1, NC * 32);
-    // sum the KS slices and store rows r < R (final output, or this CTA's partial slot)
+    if (warp < 2) {
+      const float* ob = obuf + warp * FRAG;
+#pragma unroll
+      for (int i = 0; i < MD16; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[i][e] += ob[(i * 4 + e) * 32 + lane];
+    }
+    named_bar_sync(1, NC * 32);
+    if (warp == 1) {
+#pragma unroll
+      for (int i = 0; i < MD16; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) obuf[(i * 4 + e) * 32 + lane] = o[i][e];
+    }
+    named_bar_sync(1, NC * 32);
+    // warp 0 stores rows r < R (final output, or this CTA's partial slot)
     const bool complete = sg.complete();
     const int slot_base = blockIdx.x * 2 + slot_of(sg.ustart, blockIdx.x, total, G);
-    for (int idx = threadIdx.x; idx < p.R * D; idx += NC * 32) {
-      const int r = idx / D, dd = idx - r * D;
-      float acc = 0.f;
+    if (warp == 0) {
 #pragma unroll
-      for (int k = 0; k < KS; ++k) acc += obuf[((size_t)k * D + dd) * OSTR + r];
-      const float lse2 = lsebuf[r];
-      if (complete) {
-        const int64_t orow = out_row(p, sg.b, sg.kvh, r);
-        p.out[orow * D + dd] = acc;
-        if (dd == 0 && p.lse != nullptr) p.lse[orow] = lse2 * LN2;
-      } else {
-        const int64_t prow = (int64_t)slot_base * p.R + r;
-        __stcg(p.ws_o + prow * D + dd, acc);
-        if (dd == 0) __stcg(p.ws_lse + prow, lse2);
-      }
+      for (int i = 0; i < MD16; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float v = o[i][e] + obuf[(i * 4 + e) * 32 + lane];
+          const int r = 2 * cq + (e & 1), dd = i * 16 + gq + ((e >> 1) << 3);
+          if (r >= p.R) continue;
+          if (complete) {
+            const int64_t orow = out_row(p, sg.b, sg.kvh, r);
+            p.out[orow * D + dd] = v;
+            if (dd == 0 && p.lse != nullptr) p.lse[orow] = lsebuf[r] * LN2;
+          } else {
+            const int64_t prow = (int64_t)slot_base * p.R + r;
+            __stcg(p.ws_o + prow * D + dd, v);
+            if (dd == 0) __stcg(p.ws_lse + prow, lsebuf[r]);
+          }
+        }
     }
     if (!complete) finish_unit<D>(p, sg, total, NC * 32, flag);
     named_bar_sync(1, NC * 32);  // the epilogue buffers are reused by the next segment
+    trace_stamp(p, 5);
   }
 }
 
@@ -1057,7 +1105,7 @@ static md_status launch_rows(const TmapSet& tm, const AttnParams& p, int grid, c
   static int done = -1;
   md_status st = set_smem(kern, smem, &done);
   if (st != MD_OK) return st;
-  kern<<<grid, (MT * KS + 1) * 32, smem, s>>>(tm, p);
+  if (launch_pdl(kern, grid, (MT * KS + 1) * 32, smem, s, tm, p) != cudaSuccess) return check_launch("attn_rows_kernel");
   return check_launch("attn_rows_kernel");
 }
 
@@ -1068,7 +1116,7 @@ static md_status launch_keys(const TmapSet& tm, const AttnParams& p, int grid, c
   static int done = -1;
   md_status st = set_smem(kern, C::SMEM, &done);
   if (st != MD_OK) return st;
-  kern<<<grid, C::THREADS, C::SMEM, s>>>(tm, p);
+  if (launch_pdl(kern, grid, C::THREADS, C::SMEM, s, tm, p) != cudaSuccess) return check_launch("attn_keys_kernel");
   return check_launch("attn_keys_kernel");
 }
 
@@ -1095,6 +1143,9 @@ static md_status check_cache(const md_kv_cache* c, const char* who) {
   MD_REQUIRE(aligned16(c->k) && aligned16(c->v), MD_ERR_INVALID_ARG, "%s: cache must be 16-byte aligned", who);
   return MD_OK;
 }
+
+static unsigned long long* g_trace = nullptr;  // md_debug_trace
+static size_t g_trace_bytes = 0;
 
 struct IndexedArgs {
   const int32_t* idx = nullptr;
@@ -1154,6 +1205,7 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.idx_stride = ix.idx_stride;
   p.idx_count = ix.idx_count;
   p.tail_start = ix.tail_start;
+  p.trace = (g_trace != nullptr && g_trace_bytes >= (size_t)grid * 8 * 8) ? g_trace : nullptr;
   p.row_sB = c->stride_b / c->head_dim;
   p.row_sH = c->stride_h / c->head_dim;
   p.row_sS = c->stride_s / c->head_dim;
@@ -1223,4 +1275,10 @@ extern "C" md_status md_draft_attn_indexed(const md_kv_cache* cache, const void*
   ix.tail_start = tail_start;
   return run_attention(cache, q, num_q_heads, 1, kv_len, 0, 0, MODE_INDEXED, scale, out, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_draft_attn_indexed", ix);
+}
+
+extern "C" MD_API md_status md_debug_trace(void* buf, size_t bytes) {
+  md::g_trace = static_cast<unsigned long long*>(buf);
+  md::g_trace_bytes = bytes;
+  return MD_OK;
 }

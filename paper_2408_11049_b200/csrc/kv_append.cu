@@ -2,6 +2,7 @@
 // (SURVEY §8(a) row a1).  Pure bandwidth: one thread moves one 16-byte vector, the
 // source [B][T][Hkv][d] is read fully coalesced and each destination row (d bf16 =
 // 128/256 B) is written contiguously.
+#include "md_common.cuh"
 #include "md_internal.h"
 
 namespace md {
@@ -11,6 +12,8 @@ __global__ void __launch_bounds__(256) kv_append_kernel(uint16_t* __restrict__ k
                                                         const uint16_t* __restrict__ vn,
                                                         const int32_t* __restrict__ start, int T, int Hkv, int d,
                                                         int64_t sB, int64_t sH, int64_t sS, int64_t nvec) {
+  pdl_trigger();
+  pdl_wait();
   const int vec_per_row = d >> 3;  // 8 bf16 per 16-byte vector
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / vec_per_row;  // row of [B][T][Hkv]
@@ -50,9 +53,9 @@ extern "C" md_status md_kv_append(const md_kv_cache* c, const void* k_new, const
   int64_t blocks = (nvec + threads - 1) / threads;
   const int64_t cap_blocks = (int64_t)device_sm_count() * 16;
   if (blocks > cap_blocks) blocks = cap_blocks;
-  kv_append_kernel<<<static_cast<unsigned>(blocks), threads, 0, (cudaStream_t)stream>>>(
-      static_cast<uint16_t*>(c->k), static_cast<uint16_t*>(c->v), static_cast<const uint16_t*>(k_new),
-      static_cast<const uint16_t*>(v_new), start_pos, T, c->num_kv_heads, c->head_dim, c->stride_b, c->stride_h,
-      c->stride_s, nvec);
+  launch_pdl(kv_append_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0, (cudaStream_t)stream,
+             static_cast<uint16_t*>(c->k), static_cast<uint16_t*>(c->v), static_cast<const uint16_t*>(k_new),
+             static_cast<const uint16_t*>(v_new), start_pos, (int)T, (int)c->num_kv_heads, (int)c->head_dim,
+             (int64_t)c->stride_b, (int64_t)c->stride_h, (int64_t)c->stride_s, nvec);
   return check_launch("md_kv_append");
 }

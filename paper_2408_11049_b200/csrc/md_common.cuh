@@ -140,3 +140,29 @@ MD_DEV void tma_gather4(void* dst, const void* tmap, uint64_t* bar, int col, int
       : "memory");
 }
 }  // namespace md
+
+namespace md {
+// L2 prefetch of a 4-D tensor tile (no smem, no mbarrier): raises memory-level parallelism
+// beyond the smem ring depth.
+MD_DEV void tma_prefetch_4d(const void* tmap, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+}  // namespace md
+
+namespace md {
+// Programmatic dependent launch: let the next kernel in the stream start launching now, and
+// (before touching memory an earlier kernel may have written) wait for the previous grid.
+MD_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+MD_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+}  // namespace md
+
+namespace md {
+MD_DEV uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+}  // namespace md

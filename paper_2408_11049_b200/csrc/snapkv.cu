@@ -108,6 +108,8 @@ __device__ __forceinline__ void tile_scores(const uint32_t (&qa)[D / 16][4], uin
 template <int D>
 __global__ void __launch_bounds__(THREADS) lse_kernel(const Params p) {
   __shared__ __align__(1024) uint8_t ktile[KT * D * 2];
+  pdl_trigger();
+  pdl_wait();
   const int unit = blockIdx.x / p.nchunks, chunk = blockIdx.x - unit * p.nchunks;
   const int b = unit / p.Hkv, h = unit - b * p.Hkv;
   const int L = __ldg(p.L + b);
@@ -176,6 +178,8 @@ __global__ void __launch_bounds__(THREADS) vote_kernel(const Params p) {
   __shared__ __align__(1024) uint8_t ktile[KT * D * 2];
   __shared__ float lse_s[256];
   __shared__ float wsum[WARPS][KT];
+  pdl_trigger();
+  pdl_wait();  // the chunk partials come from lse_kernel
   const int unit = blockIdx.x / p.nchunks, chunk = blockIdx.x - unit * p.nchunks;
   const int b = unit / p.Hkv, h = unit - b * p.Hkv;
   const int L = __ldg(p.L + b);
@@ -270,6 +274,8 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const Params p) {
   __shared__ uint32_t hist[256];
   __shared__ uint32_t scan_sm[SEL_THREADS / 32];
   __shared__ uint32_t s_prefix, s_need;
+  pdl_trigger();
+  pdl_wait();
   const int unit = blockIdx.x;
   const int b = unit / p.Hkv, h = unit - b * p.Hkv;
   const int n = __ldg(p.L + b) - p.w;  // prefix positions
@@ -407,12 +413,12 @@ extern "C" MD_API md_status md_snapkv_select(const md_kv_cache* c, const void* q
   cudaStream_t s = (cudaStream_t)stream;
   const unsigned grid = static_cast<unsigned>(units * p.nchunks);
   if (c->head_dim == 128) {
-    snap::lse_kernel<128><<<grid, snap::THREADS, 0, s>>>(p);
-    snap::vote_kernel<128><<<grid, snap::THREADS, 0, s>>>(p);
+    launch_pdl(snap::lse_kernel<128>, dim3(grid), dim3(snap::THREADS), 0, s, p);
+    launch_pdl(snap::vote_kernel<128>, dim3(grid), dim3(snap::THREADS), 0, s, p);
   } else {
-    snap::lse_kernel<64><<<grid, snap::THREADS, 0, s>>>(p);
-    snap::vote_kernel<64><<<grid, snap::THREADS, 0, s>>>(p);
+    launch_pdl(snap::lse_kernel<64>, dim3(grid), dim3(snap::THREADS), 0, s, p);
+    launch_pdl(snap::vote_kernel<64>, dim3(grid), dim3(snap::THREADS), 0, s, p);
   }
-  snap::select_kernel<<<static_cast<unsigned>(units), snap::SEL_THREADS, 0, s>>>(p);
+  launch_pdl(snap::select_kernel, dim3(static_cast<unsigned>(units)), dim3(snap::SEL_THREADS), 0, s, p);
   return check_launch("md_snapkv_select");
 }

@@ -39,6 +39,8 @@ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint3
 }
 
 __global__ void philox_kernel(uint64_t seed, uint64_t step, int B, int words, uint32_t* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int blocks_per_seq = (words + 3) / 4;
   const int64_t total = (int64_t)B * blocks_per_seq;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -228,6 +230,8 @@ __global__ void __launch_bounds__(ACC_THREADS) spec_accept_kernel(
     const uint32_t* __restrict__ rnd, int gamma, int V, int mode, int32_t* __restrict__ out_tokens,
     int32_t* __restrict__ num_accepted, int32_t* __restrict__ committed_len) {
   __shared__ Smem sm;
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x, tid = threadIdx.x;
   const int64_t Vl = V;
   const float* pb = p + (int64_t)b * (gamma + 1) * Vl;
@@ -302,8 +306,8 @@ extern "C" md_status md_philox_u32(uint64_t seed, uint64_t step, int32_t B, int3
   const int threads = 256;
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 4096) blocks = 4096;
-  philox_kernel<<<static_cast<unsigned>(blocks), threads, 0, (cudaStream_t)stream>>>(seed, step, B, words_per_seq,
-                                                                                      out);
+  launch_pdl(philox_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0, (cudaStream_t)stream, seed, step,
+             (int)B, (int)words_per_seq, out);
   return check_launch("md_philox_u32");
 }
 
@@ -321,8 +325,7 @@ extern "C" md_status md_spec_accept(const float* p, const float* q, const int32_
   MD_REQUIRE(mode == MD_ACCEPT_GREEDY || rnd != nullptr, MD_ERR_INVALID_ARG, "md_spec_accept: NULL rnd (SAMPLE)");
   MD_REQUIRE(mode == MD_ACCEPT_GREEDY || gamma == 0 || q != nullptr, MD_ERR_INVALID_ARG,
              "md_spec_accept: NULL q (SAMPLE)");
-  spec_accept_kernel<<<B, ACC_THREADS, 0, (cudaStream_t)stream>>>(p, q, draft_tokens, rnd, gamma, V,
-                                                                   static_cast<int>(mode), out_tokens, num_accepted,
-                                                                   committed_len_inout);
+  launch_pdl(spec_accept_kernel, dim3(B), dim3(ACC_THREADS), 0, (cudaStream_t)stream, p, q, draft_tokens, rnd,
+             (int)gamma, (int)V, static_cast<int>(mode), out_tokens, num_accepted, committed_len_inout);
   return check_launch("md_spec_accept");
 }

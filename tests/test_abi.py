@@ -82,3 +82,12 @@ def test_cpu_tensor_is_rejected():
     import torch
     with pytest.raises(ValueError):
         md._ptr(torch.zeros(4))
+
+
+def test_every_binding_declares_its_argtypes():
+    """ctypes would otherwise pass Python ints as 32-bit C ints (truncating pointers)."""
+    lib = md.load_library()
+    for name in md.ABI_SYMBOLS:
+        if name in ("md_abi_version", "md_last_error"):
+            continue
+        assert getattr(lib, name).argtypes is not None, name

@@ -1,4 +1,4 @@
-timeout 300 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"attn_keys" -s 1 -c 1 -o gpurun_out/prof_draft_v8 python tools/profile_target.py llama3_b64_32k 3 > gpurun_out/ncu_draft_v8.txt 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"attn_rows" -s 1 -c 1 -o gpurun_out/prof_qwen_v8 python tools/profile_target.py qwen_100k 2 > gpurun_out/ncu_qwen_v8.txt 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"attn_rows" -s 1 -c 1 -o gpurun_out/prof_verify_v8 python tools/profile_target.py llama3_b64_32k 2 > gpurun_out/ncu_verify_v8.txt 2>&1
-tail -1 gpurun_out/ncu_draft_v8.txt gpurun_out/ncu_qwen_v8.txt gpurun_out/ncu_verify_v8.txt
+timeout 120 python tools/trace_probe.py draft 1020 > gpurun_out/trace.txt 2>&1
+timeout 120 python tools/trace_probe.py draft 60 >> gpurun_out/trace.txt 2>&1
+timeout 120 python tools/trace_probe.py verify >> gpurun_out/trace.txt 2>&1
+cat gpurun_out/trace.txt
