@@ -125,14 +125,19 @@ def run_gpu(args):
     import paper_2408_11049_b200 as md
     import synth as S
     import synth.cuda as SC
-    from paper_2408_11049_b200.tp import gather_heads, head_shard
+    from paper_2408_11049_b200.tp import gather_rank_major, head_shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; LOCAL_RANK wraps only when testing several ranks on fewer GPUs
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("MD_DIST_BACKEND", "nccl")   # gloo only for single-GPU smoke tests
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     md.load_library()
 
     B, Hq_full, Hkv_full, d, ctx, gamma, sink, window, V, layers, alpha = CONFIGS[args.config]
@@ -208,13 +213,13 @@ def run_gpu(args):
                 md.kv_append(kb, vb, knew_d, vnew_d, pos[j])
                 md.draft_attn_sparse(qd, kb, vb, pos[j + 1], sink, window, scale, out_d, lse_d, ws_d)
                 if world > 1:
-                    gather_heads(out_d, world, buf=gath_d)
+                    gather_rank_major(out_d, gath_d)
         for l in range(layers):
             kb, vb = kc[l % R], vc[l % R]
             md.kv_append(kb, vb, knew_v, vnew_v, pos[0])
             md.verify_attn_full(qv, kb, vb, pos[gamma + 1], max_kv, scale, out_v, lse_v, ws_v)
             if world > 1:
-                gather_heads(out_v, world, buf=gath_v)
+                gather_rank_major(out_v, gath_v)
 
     # per layer-call: md_kv_append + one attention kernel (stream-K, merge fused); + philox + accept
     launches_per_step = gamma * layers * 2 + layers * 2 + 2
@@ -373,13 +378,13 @@ def run_gpu(args):
                     md.kv_append(kb, vb_, k_, v_, pos_buf[j])
                     md.draft_attn_sparse(q_, kb, vb_, pos_buf[j + 1], sink, window, scale, out_d, lse_d, ws_d)
                     if world > 1:
-                        gather_heads(out_d, world, buf=gath_d)
+                        gather_rank_major(out_d, gath_d)
                 else:
                     q_, k_, v_ = st_v[sl]
                     md.kv_append(kb, vb_, k_, v_, pos_buf[0])
                     md.verify_attn_full(q_, kb, vb_, pos_buf[gamma + 1], max_kv, scale, out_v, lse_v, ws_v)
                     if world > 1:
-                        gather_heads(out_v, world, buf=gath_v)
+                        gather_rank_major(out_v, gath_v)
                 done[sl].record(cur)
                 if c + 2 < ncalls:
                     issue_copy(c + 2)

@@ -67,6 +67,7 @@ struct AttnParams {
   int idx_stride;
   int64_t row_sB, row_sH, row_sS;  // cache strides in units of rows (d elements), for gather4
   unsigned long long* trace;       // diagnostics: [G][8] globaltimer stamps (md_debug_trace), or null
+  int fused_merge;        // 1: the last CTA of a split unit merges (acq_rel counter); 0: attn_merge_kernel
   int mode;
   float scale_log2;       // scale * log2(e)
 };
@@ -229,7 +230,14 @@ __device__ __forceinline__ int slot_of(int64_t ustart, int c, int64_t total, int
 
 // diagnostics: consumer warp 0 / lane 0 stamps phase k of this CTA (md_debug_trace)
 __device__ __forceinline__ void trace_stamp(const AttnParams& p, int k) {
-  if (p.trace != nullptr && threadIdx.x == 0) p.trace[blockIdx.x * 8 + k] = globaltimer();
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    p.trace[blockIdx.x * 8 + k] = globaltimer();
+    if (k == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      p.trace[blockIdx.x * 8 + 6] = smid;
+    }
+  }
 }
 
 __device__ __forceinline__ int64_t out_row(const AttnParams& p, int b, int kvh, int r) {
@@ -347,6 +355,55 @@ __device__ void finish_unit(const AttnParams& p, const Seg& sg, int64_t total, i
     }
     const float inv = W > 0.f ? 1.f / W : 0.f;
     const int64_t orow = out_row(p, sg.b, sg.kvh, r);
+    *reinterpret_cast<float4*>(p.out + orow * D + c4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    if (c4 == 0 && p.lse != nullptr) p.lse[orow] = (W > 0.f) ? (M + __log2f(W)) * LN2 : -INFINITY;
+  }
+}
+
+// Separate split merge (fused_merge == 0): one CTA per unit, launched right after the
+// attention kernel with programmatic dependent launch; units held whole by one CTA exit.
+template <int D>
+__global__ void __launch_bounds__(128) attn_merge_kernel(const AttnParams p, int grid_attn) {
+  __shared__ int pre[TABLE_B + 1];
+  pdl_trigger();
+  pdl_wait();  // the attention kernel's partials
+  build_prefix(p, pre);
+  const int64_t total = total_tiles(p, pre);
+  if (total == 0) return;
+  const int G = total < (int64_t)grid_attn ? static_cast<int>(total) : grid_attn;
+  const int unit = blockIdx.x, b = unit / p.Hkv, kvh = unit - b * p.Hkv;
+  int64_t bstart = 0;
+  if (p.B <= TABLE_B) {
+    bstart = pre[b];
+  } else {
+    for (int bb = 0; bb < b; ++bb) bstart += (int64_t)unit_tiles(p, bb) * p.Hkv;
+  }
+  const int tiles = tiles_of(p, pre, b);
+  if (tiles == 0) return;
+  const int64_t ustart = bstart + (int64_t)kvh * tiles;
+  const int cf = cta_of(ustart, total, G), cl = cta_of(ustart + tiles - 1, total, G);
+  if (cf == cl) return;  // written whole by one CTA
+  constexpr int V4 = D / 4;
+  for (int idx = threadIdx.x; idx < p.R * V4; idx += blockDim.x) {
+    const int r = idx / V4, c4 = (idx - r * V4) * 4;
+    float M = -INFINITY;
+    for (int c = cf; c <= cl; ++c) M = fmaxf(M, p.ws_lse[((int64_t)c * 2 + slot_of(ustart, c, total, G)) * p.R + r]);
+    float W = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = cf; c <= cl; ++c) {
+      const int64_t prow = ((int64_t)c * 2 + slot_of(ustart, c, total, G)) * p.R + r;
+      const float ls = p.ws_lse[prow];
+      if (ls == -INFINITY) continue;
+      const float w = ex2(ls - M);
+      W += w;
+      const float4 v = *reinterpret_cast<const float4*>(p.ws_o + prow * D + c4);
+      acc.x += w * v.x;
+      acc.y += w * v.y;
+      acc.z += w * v.z;
+      acc.w += w * v.w;
+    }
+    const float inv = W > 0.f ? 1.f / W : 0.f;
+    const int64_t orow = out_row(p, b, kvh, r);
     *reinterpret_cast<float4*>(p.out + orow * D + c4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     if (c4 == 0 && p.lse != nullptr) p.lse[orow] = (W > 0.f) ? (M + __log2f(W)) * LN2 : -INFINITY;
   }
@@ -661,7 +718,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
         if (c4 == 0) __stcg(p.ws_lse + prow, lse2);
       }
     }
-    if (!complete) finish_unit<D>(p, sg, total, NC * 32, flag);
+    if (!complete && p.fused_merge) finish_unit<D>(p, sg, total, NC * 32, flag);
     fence_proxy_async();         // order our generic writes to the ring before later TMA writes
     named_bar_sync(1, NC * 32);  // the scratch (= ring) may now be refilled
     if (lane == 0) mbar_arrive(epi_done);
@@ -1005,7 +1062,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
           }
         }
     }
-    if (!complete) finish_unit<D>(p, sg, total, NC * 32, flag);
+    if (!complete && p.fused_merge) finish_unit<D>(p, sg, total, NC * 32, flag);
     named_bar_sync(1, NC * 32);  // the epilogue buffers are reused by the next segment
     trace_stamp(p, 5);
   }
@@ -1022,6 +1079,15 @@ static int keys_ctas_per_sm() {
   static const int v = [] {
     const char* e = getenv("MD_KEYS_CTAS");
     return (e && atoi(e) == 1) ? 1 : 2;
+  }();
+  return v;
+}
+
+// split merge: fused in the attention kernel (default) or a PDL-launched kernel (MD_MERGE=kernel)
+static int fused_merge_enabled() {
+  static const int v = [] {
+    const char* e = getenv("MD_MERGE");
+    return (e && std::string(e) == "kernel") ? 0 : 1;
   }();
   return v;
 }
@@ -1206,6 +1272,7 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.idx_count = ix.idx_count;
   p.tail_start = ix.tail_start;
   p.trace = (g_trace != nullptr && g_trace_bytes >= (size_t)grid * 8 * 8) ? g_trace : nullptr;
+  p.fused_merge = fused_merge_enabled();
   p.row_sB = c->stride_b / c->head_dim;
   p.row_sH = c->stride_h / c->head_dim;
   p.row_sS = c->stride_s / c->head_dim;
@@ -1215,7 +1282,13 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.ws_lse = reinterpret_cast<float*>(w);
   w += align256((size_t)grid * 2 * R * 4);
   p.counters = reinterpret_cast<int*>(w);
-  return (c->head_dim == 128) ? launch_dim<128>(tm, p, grid, s) : launch_dim<64>(tm, p, grid, s);
+  st = (c->head_dim == 128) ? launch_dim<128>(tm, p, grid, s) : launch_dim<64>(tm, p, grid, s);
+  if (st != MD_OK || p.fused_merge) return st;
+  if (c->head_dim == 128)
+    launch_pdl(attn_merge_kernel<128>, dim3(units), dim3(128), 0, s, p, grid);
+  else
+    launch_pdl(attn_merge_kernel<64>, dim3(units), dim3(128), 0, s, p, grid);
+  return check_launch("attn_merge_kernel");
 }
 
 }  // namespace md

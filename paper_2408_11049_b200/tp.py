@@ -23,6 +23,15 @@ def head_shard(Hq: int, Hkv: int, rank: int, world: int):
     return slice(rank * kv_per * g, (rank + 1) * kv_per * g), slice(rank * kv_per, (rank + 1) * kv_per)
 
 
+def gather_rank_major(out_local: torch.Tensor, buf: torch.Tensor, group=None) -> torch.Tensor:
+    """The exchange itself: all-gather rank-local outputs into a rank-major [P, ...] buffer
+    (one NCCL all_gather_into_tensor; the o_proj input can be consumed rank-major)."""
+    world = buf.shape[0]
+    flat = buf.view((world * out_local.shape[0],) + tuple(out_local.shape[1:]))
+    dist.all_gather_into_tensor(flat, out_local, group=group)
+    return buf
+
+
 def gather_heads(out_local: torch.Tensor, world: int, group=None, buf: torch.Tensor | None = None) -> torch.Tensor:
     """All-gather rank-local outputs [..., Hq/P, d] along the head axis -> [..., Hq, d].
 

@@ -63,3 +63,5 @@ res["span_end_minus_entry_p50"] = round(float(np.median(rel[:, 5] - rel[:, 0])),
 res["first_tile_minus_located_p50"] = round(float(np.median(rel[:, 3] - rel[:, 2])), 2)
 res["tail_last_epilogue_to_end_p50"] = round(float(np.median(rel[:, 5] - rel[:, 4])), 2)
 print(json.dumps(res))
+raw = trace.cpu().numpy()[: len(t)]
+np.save(os.path.join("gpurun_out", f"trace_{mode}_{window}.npy"), raw)
