@@ -19,6 +19,10 @@
  *   md_spec_accept        batched acceptance + residual / bonus resampling (or greedy)
  *   md_philox_u32         counter-based uniforms feeding md_spec_accept
  *
+ * Tree-based speculation (P:173 names token trees as compatible with
+ * the analysis): md_verify_attn_tree (tree-masked verify), md_spec_accept_tree (recursive
+ * rejection over siblings) and md_kv_compact (move the accepted path's K/V rows together).
+ *
  * Conventions shared by every call
  *   - Every pointer argument named as "device" is caller-owned CUDA device memory;
  *     the library never allocates, frees, synchronises or copies host<->device.
@@ -139,6 +143,23 @@ MD_API md_status md_verify_attn_full(const md_kv_cache* cache, const void* q, in
                               void* workspace, size_t workspace_bytes, md_stream_t stream);
 
 /*
+ * md_verify_attn_tree — verification of a token TREE of T nodes per sequence (f3; the
+ * chain of md_verify_attn_full is the special case tree_mask[b][t] = 2^(t+1) - 1).
+ * Node t's K/V row sits at cache position n - T + t (node 0 = the pending root token),
+ * parent[t] < t.  For b < B, t < T, h < Hq, with n = kv_len[b]:
+ *     J = [0, n - T)  ∪  { n - T + j : bit j of tree_mask[b][t] is set }
+ * (for a tree: the ancestors-or-self of node t, mask[t] = mask[parent[t]] | 1 << t),
+ * otherwise exactly md_verify_attn_full (same outputs, workspace and limits).
+ *   tree_mask: device uint32 [B][T]; bits >= T are ignored.
+ * Preconditions (device): a row whose J is empty (only possible when n = T and its mask is
+ * 0) gets out = 0, lse = -inf.
+ */
+MD_API md_status md_verify_attn_tree(const md_kv_cache* cache, const void* q, int32_t num_q_heads, int32_t T,
+                              const int32_t* kv_len, int32_t max_kv_len, const uint32_t* tree_mask, float scale,
+                              float* out, float* lse, void* workspace, size_t workspace_bytes,
+                              md_stream_t stream);
+
+/*
  * md_draft_attn_sparse — self-speculative draft attention over the StreamingLLM
  * compressed KV ("StreamingLLM style sparse KV for drafting", P:460 budgets,
  * P:720 static compressed KV; Eq.3 P:1081 with T_select = 0 for a static method).
@@ -243,6 +264,47 @@ MD_API md_status md_philox_u32(uint64_t seed, uint64_t step, int32_t B, int32_t 
 MD_API md_status md_spec_accept(const float* p, const float* q, const int32_t* draft_tokens, const uint32_t* rnd,
                          int32_t B, int32_t gamma, int32_t V, md_accept_mode mode, int32_t* out_tokens,
                          int32_t* num_accepted, int32_t* committed_len_inout, md_stream_t stream);
+
+/*
+ * md_spec_accept_tree — acceptance over a token tree (f3; readings Z21-Z24).
+ * Node 0 is the root (the pending token), parent[b][t] < t for t >= 1; tokens[b][t] is
+ * node t's token (tokens[b][0] is not read); p[b][t] / q[b][t] are the target / draft
+ * distributions AT node t (over node t's children).  Walk from cur = 0:
+ *   SAMPLE: children c of cur are tested in index order, test word rnd[b][k] for the k-th
+ *     test overall (m = rnd >> 3).  First child: m q_cur(x) < p_cur(x) 2^29 (fp64, as
+ *     md_spec_accept).  After its rejection R = max(0, P - Q) on the 2^-40 grid (P =
+ *     floor(p_cur 2^40), Q = floor(q_cur 2^40); R = P if that sums to 0); each later
+ *     sibling x is accepted iff m Q_x S < R_x 2^69 (S = sum R, exact integers; rejected if
+ *     S = 0), a rejection updating R_i <- max(0, floor(R_i 2^40 / S) - Q_i) (kept if that
+ *     sums to 0).  An accepted child becomes cur.  When every child is rejected the new
+ *     token is drawn from R, at a leaf from P (argmax p_cur if the weights sum to 0), with
+ *     u = rnd[b][T-1] << 32 | rnd[b][T] exactly as md_spec_accept.
+ *   GREEDY: a = lowest-index argmax p_cur; move to the lowest-index child whose token is a,
+ *     else emit a.  q and rnd are not read.
+ * For a chain (parent[t] = t - 1) this equals md_spec_accept bit for bit.
+ * Outputs: out_tokens[b] = [path tokens..., new, -1 ...] (T entries), num_accepted[b] =
+ * path length n, accepted_nodes[b] = [path node indices..., -1 ...] (T entries; may be
+ * NULL), committed_len[b] += n + 1 if committed_len_inout != NULL.
+ *   p, q: device fp32 [B][T][V]; tokens, parent: device int32 [B][T];
+ *   rnd: device uint32 [B][T+1].  Supported: 1 <= T <= 16.
+ */
+MD_API md_status md_spec_accept_tree(const float* p, const float* q, const int32_t* tokens, const int32_t* parent,
+                              const uint32_t* rnd, int32_t B, int32_t T, int32_t V, md_accept_mode mode,
+                              int32_t* out_tokens, int32_t* num_accepted, int32_t* accepted_nodes,
+                              int32_t* committed_len_inout, md_stream_t stream);
+
+/*
+ * md_kv_compact — after tree acceptance, move the K/V rows of the accepted path next to
+ * the root: for every b, kv head h and i < count[b], row base[b] + nodes[b][i] is copied
+ * to base[b] + 1 + i (all reads happen before any write of a (b, h), so overlapping sets
+ * are safe).  base[b] = the root's position (n - T); nodes is md_spec_accept_tree's
+ * accepted_nodes, count its num_accepted.
+ *   base, count: device int32 [B]; nodes: device int32 [B][nodes_stride].
+ * Supported: 1 <= nodes_stride <= 16, head_dim a multiple of 8 up to 256.
+ * Preconditions (device): count[b] <= nodes_stride, base[b] + nodes[b][i] < capacity.
+ */
+MD_API md_status md_kv_compact(const md_kv_cache* cache, const int32_t* base, const int32_t* nodes,
+                        int32_t nodes_stride, const int32_t* count, md_stream_t stream);
 
 /*
  * md_debug_trace — diagnostics only.  While `buf` (device uint64 [G][8], G = CTAs of the

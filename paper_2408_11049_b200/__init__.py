@@ -7,7 +7,8 @@ tensor raises.
 
 Functions mirror the C calls (same names without the `md_` prefix):
     kv_append, attn_workspace_bytes, verify_attn_full, draft_attn_sparse,
-    draft_attn_indexed, snapkv_workspace_bytes, snapkv_select, philox_u32, spec_accept
+    draft_attn_indexed, snapkv_workspace_bytes, snapkv_select, philox_u32, spec_accept,
+    verify_attn_tree, spec_accept_tree, kv_compact (tree speculation)
 """
 from __future__ import annotations
 
@@ -25,7 +26,8 @@ MD_ACCEPT_SAMPLE, MD_ACCEPT_GREEDY = 0, 1
 # the symbols include/magicdec_b200.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_workspace_bytes",
                "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed", "md_snapkv_workspace_bytes",
-               "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace")
+               "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace",
+               "md_verify_attn_tree", "md_spec_accept_tree", "md_kv_compact")
 
 
 class MDError(RuntimeError):
@@ -76,8 +78,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.md_spec_accept.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, i32, i32, i32, ctypes.c_int,
                                    c_void_p, c_void_p, c_void_p, c_void_p]
     lib.md_debug_trace.argtypes = [c_void_p, sz]
+    lib.md_verify_attn_tree.argtypes = [pc, c_void_p, i32, i32, c_void_p, i32, c_void_p, f32, c_void_p, c_void_p,
+                                        c_void_p, sz, c_void_p]
+    lib.md_spec_accept_tree.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, i32, i32, i32,
+                                        ctypes.c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+    lib.md_kv_compact.argtypes = [pc, c_void_p, c_void_p, i32, c_void_p, c_void_p]
     for name in ("md_kv_append", "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed",
-                 "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace"):
+                 "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace", "md_verify_attn_tree",
+                 "md_spec_accept_tree", "md_kv_compact"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -143,6 +151,17 @@ def verify_attn_full(q, k_cache, v_cache, kv_len, max_kv_len, scale, out, lse=No
                                    float(scale), _ptr(out), _ptr(lse), ws, wsb, _stream(stream)))
 
 
+def verify_attn_tree(q, k_cache, v_cache, kv_len, max_kv_len, tree_mask, scale, out, lse=None, workspace=None,
+                     stream=None):
+    """Tree verify: q [B, T, Hq, d] bf16, tree_mask [B, T] (int32 storage of uint32; bit j of (b, t) =
+    node t sees node j) -> out [B, T, Hq, d] fp32 (and lse [B, T, Hq])."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_verify_attn_tree(ctypes.byref(c), _ptr(q), q.shape[2], q.shape[1], _ptr(kv_len), int(max_kv_len),
+                                   _ptr(tree_mask), float(scale), _ptr(out), _ptr(lse), ws, wsb, _stream(stream)))
+
+
 def draft_attn_sparse(q, k_cache, v_cache, kv_len, sink, window, scale, out, lse=None, workspace=None, stream=None):
     """q [B, Hq, d] bf16 over the sink + window rows -> out [B, Hq, d] fp32 (and lse [B, Hq])."""
     lib = load_library()
@@ -199,6 +218,26 @@ def spec_accept(p, q, draft_tokens, rnd, out_tokens, num_accepted, committed_len
     m = MD_ACCEPT_SAMPLE if mode == "sample" else MD_ACCEPT_GREEDY
     _check(lib.md_spec_accept(_ptr(p), _ptr(q), _ptr(draft_tokens), _ptr(rnd), B, G1 - 1, V, m, _ptr(out_tokens),
                               _ptr(num_accepted), _ptr(committed_len), _stream(stream)))
+
+
+def spec_accept_tree(p, q, tokens, parent, rnd, out_tokens, num_accepted, accepted_nodes=None, committed_len=None,
+                     mode="sample", stream=None):
+    """Tree acceptance.  p, q [B, T, V] fp32 (distributions at each node), tokens / parent [B, T] int32,
+    rnd [B, T+1] -> out_tokens [B, T], num_accepted [B], accepted_nodes [B, T]."""
+    lib = load_library()
+    B, T, V = p.shape
+    m = MD_ACCEPT_SAMPLE if mode == "sample" else MD_ACCEPT_GREEDY
+    _check(lib.md_spec_accept_tree(_ptr(p), _ptr(q), _ptr(tokens), _ptr(parent), _ptr(rnd), B, T, V, m,
+                                   _ptr(out_tokens), _ptr(num_accepted), _ptr(accepted_nodes), _ptr(committed_len),
+                                   _stream(stream)))
+
+
+def kv_compact(k_cache, v_cache, base, nodes, count, stream=None):
+    """cache[b, :, base[b] + 1 + i] = cache[b, :, base[b] + nodes[b, i]] for i < count[b]."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    _check(lib.md_kv_compact(ctypes.byref(c), _ptr(base), _ptr(nodes), nodes.shape[1], _ptr(count),
+                             _stream(stream)))
 
 
 def debug_trace(buf=None):

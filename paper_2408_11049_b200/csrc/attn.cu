@@ -68,6 +68,7 @@ struct AttnParams {
   int64_t row_sB, row_sH, row_sS;  // cache strides in units of rows (d elements), for gather4
   unsigned long long* trace;       // diagnostics: [G][8] globaltimer stamps (md_debug_trace), or null
   int fused_merge;        // 1: the last CTA of a split unit merges (acq_rel counter); 0: attn_merge_kernel
+  const uint32_t* tree_mask;  // verify: [B][T] bit j of (b, t) = node t sees new key n-T+j (null: causal chain)
   int mode;
   float scale_log2;       // scale * log2(e)
 };
@@ -82,6 +83,16 @@ __device__ __forceinline__ int unit_keys(const AttnParams& p, int n, int b) {
 __device__ __forceinline__ int unit_tiles(const AttnParams& p, int b) {
   return (unit_keys(p, __ldg(p.kv_len + b), b) + TK - 1) / TK;
 }
+// Visibility of the T new keys [n-T, n) to verify query node t: the
+// causal chain (2^(t+1) - 1) or the caller's tree mask (ancestors-or-self of node t).
+// A key at offset rel = pos - (n - T) is hidden iff rel >= 0 and bit rel is clear; draft
+// modes pass vbase = INT_MAX so rel < 0 always.
+__device__ __forceinline__ uint32_t node_mask(const AttnParams& p, int b, int row) {
+  const int t = min(row, p.R - 1) / p.g;
+  return p.tree_mask ? __ldg(p.tree_mask + (size_t)b * p.T + t) : ((2u << t) - 1u);
+}
+__device__ __forceinline__ bool key_hidden(uint32_t mask, int rel) { return rel >= 0 && !((mask >> (rel & 31)) & 1u); }
+
 // Per-CTA prefix table over sequences in shared memory: pre[b] = sum_{b' < b} Hkv * tiles(b')
 // (built once per CTA with one parallel load of kv_len, so locating a CTA's range costs a
 // binary search instead of B dependent global loads).  Batches larger than TABLE_B (256)
@@ -523,13 +534,9 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
         qa[kk][3] = q1 ? __ldg(q1 + c + 4) : 0u;
       }
     }
-    // causal limit per fragment row (verify): key j visible iff j <= n - T + t(row)
-    int lim0 = 0x7fffffff, lim1 = 0x7fffffff;
-    if (p.mode == MODE_VERIFY) {
-      lim0 = n - p.T + min(mt * 16 + gq, p.R - 1) / p.g;
-      lim1 = n - p.T + min(mt * 16 + gq + 8, p.R - 1) / p.g;
-    }
-    const int lim_warp = n - p.T;  // keys <= this are visible to every verify row
+    // visibility of the new keys per fragment row (verify): node_mask of t(row)
+    const int vbase = (p.mode == MODE_VERIFY) ? n - p.T : 0x7fffffff;  // keys < vbase: visible to all rows
+    const uint32_t msk0 = node_mask(p, b, mt * 16 + gq), msk1 = node_mask(p, b, mt * 16 + gq + 8);
 
     float o[NT_O][4];
 #pragma unroll
@@ -566,7 +573,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
             }
           }
           // ---------------- scale, mask, online softmax (log2 domain)
-          const bool need_mask = (kw0 + KW > nvalid) || (p.mode == MODE_VERIFY && pos + kw0 + KW - 1 > lim_warp);
+          const bool need_mask = (kw0 + KW > nvalid) || (pos + kw0 + KW - 1 >= vbase);
           float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
           for (int i = 0; i < NT_S; ++i) {
@@ -575,7 +582,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
               float v = s[i][e] * p.scale_log2;
               if (need_mask) {
                 const int ko = kw0 + i * 8 + cq * 2 + (e & 1);
-                v = (ko >= nvalid || pos + ko > ((e < 2) ? lim0 : lim1)) ? -INFINITY : v;
+                v = (ko >= nvalid || key_hidden((e < 2) ? msk0 : msk1, pos + ko - vbase)) ? -INFINITY : v;
               }
               s[i][e] = v;
             }
@@ -845,13 +852,12 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   while (walk.next(p, sg)) {
     const int n = sg.n;
     const Ranges rg = seg_ranges(p, sg);
-    // causal limit of the two rows 2cq, 2cq+1 this thread holds (verify; rows past R take
-    // the limit of row R-1, their output is dropped)
-    int lim[2];
+    // new-key visibility of the two rows 2cq, 2cq+1 this thread holds (verify; rows past R
+    // take the mask of row R-1, their output is dropped)
+    const int vbase = (p.mode == MODE_VERIFY) ? n - p.T : 0x7fffffff;
+    uint32_t msk[2];
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
-      lim[j] = (p.mode == MODE_VERIFY) ? n - p.T + min(2 * cq + j, p.R - 1) / p.g : 0x7fffffff;
-    const int lim_warp = n - p.T;
+    for (int j = 0; j < 2; ++j) msk[j] = node_mask(p, sg.b, 2 * cq + j);
     // Q^T fragments (B operand): qb[kk][0..1] = Q[gq][kk*16 + 2cq (+8) ..]
     uint32_t qb[MD16][2];
     {
@@ -899,7 +905,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
             }
           }
           // ---------------- scale, mask, online softmax (log2 domain); rows 2cq, 2cq+1
-          const bool need_mask = (kw0 + KW > nvalid) || (p.mode == MODE_VERIFY && pos + kw0 + KW - 1 > lim_warp);
+          const bool need_mask = (kw0 + KW > nvalid) || (pos + kw0 + KW - 1 >= vbase);
           float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
           for (int kb = 0; kb < KB; ++kb)
@@ -908,7 +914,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
               float v = s[kb][e] * p.scale_log2;
               if (need_mask) {
                 const int ko = kw0 + kb * 16 + gq + ((e >> 1) << 3);
-                v = (ko >= nvalid || pos + ko > lim[e & 1]) ? -INFINITY : v;
+                v = (ko >= nvalid || key_hidden(msk[e & 1], pos + ko - vbase)) ? -INFINITY : v;
               }
               s[kb][e] = v;
               mx[e & 1] = fmaxf(mx[e & 1], v);
@@ -1218,6 +1224,7 @@ struct IndexedArgs {
   int idx_stride = 0;
   const int32_t* idx_count = nullptr;
   const int32_t* tail_start = nullptr;
+  const uint32_t* tree_mask = nullptr;  // verify only
 };
 
 static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int T, const int32_t* kv_len, int sink,
@@ -1271,6 +1278,7 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.idx_stride = ix.idx_stride;
   p.idx_count = ix.idx_count;
   p.tail_start = ix.tail_start;
+  p.tree_mask = ix.tree_mask;
   p.trace = (g_trace != nullptr && g_trace_bytes >= (size_t)grid * 8 * 8) ? g_trace : nullptr;
   p.fused_merge = fused_merge_enabled();
   p.row_sB = c->stride_b / c->head_dim;
@@ -1314,6 +1322,22 @@ extern "C" md_status md_verify_attn_full(const md_kv_cache* cache, const void* q
              "md_verify_attn_full: need T <= max_kv_len <= capacity");
   return run_attention(cache, q, num_q_heads, T, kv_len, 0, 0, MODE_VERIFY, scale, out, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_verify_attn_full");
+}
+
+extern "C" md_status md_verify_attn_tree(const md_kv_cache* cache, const void* q, int32_t num_q_heads, int32_t T,
+                                         const int32_t* kv_len, int32_t max_kv_len, const uint32_t* tree_mask,
+                                         float scale, float* out, float* lse, void* workspace, size_t workspace_bytes,
+                                         md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(T >= 1 && T <= 16, MD_ERR_UNSUPPORTED, "md_verify_attn_tree: T must be in [1, 16]");
+  MD_REQUIRE(cache != nullptr && tree_mask != nullptr, MD_ERR_INVALID_ARG, "md_verify_attn_tree: NULL cache/mask");
+  MD_REQUIRE(max_kv_len >= T && max_kv_len <= cache->capacity, MD_ERR_INVALID_ARG,
+             "md_verify_attn_tree: need T <= max_kv_len <= capacity");
+  IndexedArgs ix;
+  ix.tree_mask = tree_mask;
+  return run_attention(cache, q, num_q_heads, T, kv_len, 0, 0, MODE_VERIFY, scale, out, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_verify_attn_tree", ix);
 }
 
 extern "C" md_status md_draft_attn_sparse(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
