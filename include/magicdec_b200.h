@@ -307,10 +307,13 @@ MD_API md_status md_kv_compact(const md_kv_cache* cache, const int32_t* base, co
                         int32_t nodes_stride, const int32_t* count, md_stream_t stream);
 
 /*
- * md_debug_trace — diagnostics only.  While `buf` (device uint64 [G][8], G = CTAs of the
- * attention grid; 0 disables) is set, every attention call stamps %globaltimer per CTA at:
- * entry, after the grid-dependency wait, after locating its stream-K range, first K/V tile
- * landed, last segment epilogue start, end.  Process-wide, not thread-safe; NULL disables.
+ * md_debug_trace — diagnostics only.  While `buf` (device uint64 [G][16], G = CTAs of the
+ * attention grid) is set, every attention call stamps %globaltimer per CTA in slots: 0 entry,
+ * 1 after the grid-dependency wait, 2 after locating its stream-K range, 3 first K/V tile
+ * landed, 4 last segment epilogue start, 5 end, 6 = the SM id, 7/8/9 last epilogue after the
+ * cross-warp combine / after its stores / after the split merge, 10 producer done,
+ * 11 = segments processed (slots 7-11: draft/keys kernel only).  Process-wide, not
+ * thread-safe; NULL disables.
  */
 MD_API md_status md_debug_trace(void* buf, size_t bytes);
 

@@ -18,7 +18,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmagicdec_b200.so")
+LIB_PATH = os.environ.get("MD_LIB") or os.path.join(_HERE, "libmagicdec_b200.so")  # MD_LIB: A/B experiments
 
 MD_OK, MD_ERR_INVALID_ARG, MD_ERR_UNSUPPORTED, MD_ERR_WORKSPACE, MD_ERR_CUDA = 0, 1, 2, 3, 4
 MD_ACCEPT_SAMPLE, MD_ACCEPT_GREEDY = 0, 1
@@ -241,6 +241,6 @@ def kv_compact(k_cache, v_cache, base, nodes, count, stream=None):
 
 
 def debug_trace(buf=None):
-    """Diagnostics: stamp per-CTA phase times of every attention call into buf (int64 [G, 8])."""
+    """Diagnostics: stamp per-CTA phase times of every attention call into buf (int64 [G, 16])."""
     lib = load_library()
     _check(lib.md_debug_trace(_ptr(buf), 0 if buf is None else buf.numel() * 8))

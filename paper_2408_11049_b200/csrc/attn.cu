@@ -68,6 +68,7 @@ struct AttnParams {
   int64_t row_sB, row_sH, row_sS;  // cache strides in units of rows (d elements), for gather4
   unsigned long long* trace;       // diagnostics: [G][8] globaltimer stamps (md_debug_trace), or null
   int fused_merge;        // 1: the last CTA of a split unit merges (acq_rel counter); 0: attn_merge_kernel
+  int warm;               // producer lanes touch each segment's output / workspace / counter early
   const uint32_t* tree_mask;  // verify: [B][T] bit j of (b, t) = node t sees new key n-T+j (null: causal chain)
   int mode;
   float scale_log2;       // scale * log2(e)
@@ -240,13 +241,21 @@ __device__ __forceinline__ int slot_of(int64_t ustart, int c, int64_t total, int
 }
 
 // diagnostics: consumer warp 0 / lane 0 stamps phase k of this CTA (md_debug_trace)
+constexpr int TRACE_SLOTS = 16;
+// Diagnostics (md_debug_trace): slot 0 entry, 1 after the grid-dependency wait, 2 range
+// located, 3 first tile landed, 4 last epilogue start, 5 end, 6 smid, 7 last epilogue after
+// the cross-warp combine, 8 after its stores, 9 after finish_unit, 10 producer done,
+// 11 segments processed.
+__device__ __forceinline__ void trace_put(const AttnParams& p, int k, unsigned long long v) {
+  if (p.trace != nullptr) p.trace[blockIdx.x * TRACE_SLOTS + k] = v;
+}
 __device__ __forceinline__ void trace_stamp(const AttnParams& p, int k) {
   if (p.trace != nullptr && threadIdx.x == 0) {
-    p.trace[blockIdx.x * 8 + k] = globaltimer();
+    trace_put(p, k, globaltimer());
     if (k == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      p.trace[blockIdx.x * 8 + 6] = smid;
+      trace_put(p, 6, smid);
     }
   }
 }
@@ -340,25 +349,29 @@ __device__ void finish_unit(const AttnParams& p, const Seg& sg, int64_t total, i
     flag[0] = last;
     flag[1] = cf;
     flag[2] = cl;
+    // the unit is the LAST segment of CTA cf iff cf's range began before it (slot 1); for
+    // every later CTA it is the first segment (slot 0)
+    flag[3] = slot_of(sg.ustart, cf, total, G);
   }
   named_bar_sync(1, nthr);
   if (!flag[0]) return;
-  const int cf = flag[1], cl = flag[2];
+  const int cf = flag[1], cl = flag[2], s0 = flag[3];
   constexpr int V4 = D / 4;
   for (int idx = threadIdx.x; idx < p.R * V4; idx += nthr) {
     const int r = idx / V4, c4 = (idx - r * V4) * 4;
     float M = -INFINITY;
+#pragma unroll 4
     for (int c = cf; c <= cl; ++c)
-      M = fmaxf(M, __ldcg(p.ws_lse + ((int64_t)c * 2 + slot_of(sg.ustart, c, total, G)) * p.R + r));
+      M = fmaxf(M, __ldcg(p.ws_lse + ((int64_t)c * 2 + (c == cf ? s0 : 0)) * p.R + r));
     float W = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
     for (int c = cf; c <= cl; ++c) {
-      const int64_t prow = ((int64_t)c * 2 + slot_of(sg.ustart, c, total, G)) * p.R + r;
+      const int64_t prow = ((int64_t)c * 2 + (c == cf ? s0 : 0)) * p.R + r;
       const float ls = __ldcg(p.ws_lse + prow);
-      if (ls == -INFINITY) continue;
-      const float w = ex2(ls - M);
-      W += w;
       const float4 v = __ldcg(reinterpret_cast<const float4*>(p.ws_o + prow * D + c4));
+      const float w = (ls == -INFINITY) ? 0.f : ex2(ls - M);  // empty partials hold finite zeros
+      W += w;
       acc.x += w * v.x;
       acc.y += w * v.y;
       acc.z += w * v.z;
@@ -452,7 +465,9 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
                 "epilogue buffer must fit in the ring");
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align to 1 KB by offsetting the __shared__ array itself, so every derived pointer keeps
+  // the shared address space (LDS/STS instead of generic loads/stores)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::RING_BYTES);
   uint64_t* empty = full + NSTAGE;
   uint64_t* epi_done = empty + NSTAGE;
@@ -769,7 +784,9 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   constexpr int MD16 = D / 16;  // m16 tiles of O^T (head-dim rows) == k16 steps of S^T
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align to 1 KB by offsetting the __shared__ array itself, so every derived pointer keeps
+  // the shared address space (LDS/STS instead of generic loads/stores)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* qbuf = smem + NSTAGE * C::STAGE;
   float* obuf = reinterpret_cast<float*>(qbuf + C::QBUF);  // [NC/2][FRAG]    O^T fragments (tree merge)
   float* mlbuf = obuf + (NC / 2) * FRAG;                    // [NC][8][2]      (m, l) per warp row
@@ -835,11 +852,16 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         mbar_arrive_expect_tx(&qfull[qs], p.R * D * 2);
         for (int r = 0; r < p.R; ++r)
           bulk_load(qbuf + (qs * C::ROWS + r) * C::QSTR, p.q + out_row(p, sg.b, sg.kvh, r) * D, D * 2, &qfull[qs]);
+      } else if (p.warm && lane < 4) {
+        if (lane == 1) touch_global(p.out + out_row(p, sg.b, sg.kvh, 0) * D);
+        if (lane == 2) touch_global(p.ws_o + (int64_t)blockIdx.x * 2 * p.R * D);
+        if (lane == 3) touch_global(p.counters + sg.unit);
       }
       __syncwarp();
       produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol);
       ++qi;
     }
+    if (lane == 0) trace_put(p, 10, globaltimer());
     return;
   }
 
@@ -849,6 +871,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   const uint32_t ring = smem_u32(smem);
   const uint32_t qring = smem_u32(qbuf);
   int it = 0, qi = 0;
+  unsigned long long qi_seg = 0;
   while (walk.next(p, sg)) {
     const int n = sg.n;
     const Ranges rg = seg_ranges(p, sg);
@@ -1021,8 +1044,11 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         o[i][3] *= f[1];
       }
     }
-    // sum the KS = 4 slices in registers by a 2-round tree through shared memory (every warp
-    // holds the same fragment layout, so lane t adds lane t's values: conflict-free)
+    // Sum the KS = 4 slices: warps 2, 3 park their fragments (every warp holds the same
+    // fragment layout, so lane t adds lane t's values: conflict-free), warps 0, 1 add them
+    // and write their sums as two row-major [8][D] planes over the same buffer (column
+    // XOR-swizzled by (r >> 1) << 3: conflict-free), then all warps add the planes and store
+    // whole rows with 16-byte vectors.
     if (warp >= 2) {
       float* ob = obuf + (warp - 2) * FRAG;
 #pragma unroll
@@ -1032,45 +1058,51 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     }
     named_bar_sync(1, NC * 32);
     if (warp < 2) {
-      const float* ob = obuf + warp * FRAG;
+      float* ob = obuf + warp * FRAG;  // FRAG == 8 * D: one plane
 #pragma unroll
       for (int i = 0; i < MD16; ++i)
 #pragma unroll
         for (int e = 0; e < 4; ++e) o[i][e] += ob[(i * 4 + e) * 32 + lane];
-    }
-    named_bar_sync(1, NC * 32);
-    if (warp == 1) {
-#pragma unroll
-      for (int i = 0; i < MD16; ++i)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) obuf[(i * 4 + e) * 32 + lane] = o[i][e];
-    }
-    named_bar_sync(1, NC * 32);
-    // warp 0 stores rows r < R (final output, or this CTA's partial slot)
-    const bool complete = sg.complete();
-    const int slot_base = blockIdx.x * 2 + slot_of(sg.ustart, blockIdx.x, total, G);
-    if (warp == 0) {
+      __syncwarp();
 #pragma unroll
       for (int i = 0; i < MD16; ++i)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float v = o[i][e] + obuf[(i * 4 + e) * 32 + lane];
           const int r = 2 * cq + (e & 1), dd = i * 16 + gq + ((e >> 1) << 3);
-          if (r >= p.R) continue;
-          if (complete) {
-            const int64_t orow = out_row(p, sg.b, sg.kvh, r);
-            p.out[orow * D + dd] = v;
-            if (dd == 0 && p.lse != nullptr) p.lse[orow] = lsebuf[r] * LN2;
-          } else {
-            const int64_t prow = (int64_t)slot_base * p.R + r;
-            __stcg(p.ws_o + prow * D + dd, v);
-            if (dd == 0) __stcg(p.ws_lse + prow, lsebuf[r]);
-          }
+          ob[r * D + (dd ^ (cq << 3))] = o[i][e];
         }
     }
+    named_bar_sync(1, NC * 32);
+    trace_stamp(p, 7);
+    // rows r < R -> the final output, or this CTA's partial slot
+    const bool complete = sg.complete();
+    const int slot_base = blockIdx.x * 2 + slot_of(sg.ustart, blockIdx.x, total, G);
+    {
+      constexpr int V4 = D / 4;
+      for (int idx = threadIdx.x; idx < p.R * V4; idx += NC * 32) {
+        const int r = idx / V4, c4 = (idx - r * V4) * 4;
+        const int sc = c4 ^ (((r >> 1) & 3) << 3);
+        const float4 a = *reinterpret_cast<const float4*>(obuf + r * D + sc);
+        const float4 c = *reinterpret_cast<const float4*>(obuf + FRAG + r * D + sc);
+        const float4 v = make_float4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
+        if (complete) {
+          const int64_t orow = out_row(p, sg.b, sg.kvh, r);
+          *reinterpret_cast<float4*>(p.out + orow * D + c4) = v;
+          if (c4 == 0 && p.lse != nullptr) p.lse[orow] = lsebuf[r] * LN2;
+        } else {
+          const int64_t prow = (int64_t)slot_base * p.R + r;
+          __stcg(reinterpret_cast<float4*>(p.ws_o + prow * D + c4), v);
+          if (c4 == 0) __stcg(p.ws_lse + prow, lsebuf[r]);
+        }
+      }
+    }
+    trace_stamp(p, 8);
     if (!complete && p.fused_merge) finish_unit<D>(p, sg, total, NC * 32, flag);
+    trace_stamp(p, 9);
     named_bar_sync(1, NC * 32);  // the epilogue buffers are reused by the next segment
     trace_stamp(p, 5);
+    ++qi_seg;
+    if (threadIdx.x == 0) trace_put(p, 11, qi_seg);
   }
 }
 
@@ -1090,6 +1122,11 @@ static int keys_ctas_per_sm() {
 }
 
 // split merge: fused in the attention kernel (default) or a PDL-launched kernel (MD_MERGE=kernel)
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 static int fused_merge_enabled() {
   static const int v = [] {
     const char* e = getenv("MD_MERGE");
@@ -1279,8 +1316,9 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.idx_count = ix.idx_count;
   p.tail_start = ix.tail_start;
   p.tree_mask = ix.tree_mask;
-  p.trace = (g_trace != nullptr && g_trace_bytes >= (size_t)grid * 8 * 8) ? g_trace : nullptr;
+  p.trace = (g_trace != nullptr && g_trace_bytes >= (size_t)grid * TRACE_SLOTS * 8) ? g_trace : nullptr;
   p.fused_merge = fused_merge_enabled();
+  p.warm = env_int("MD_WARM", 1);
   p.row_sB = c->stride_b / c->head_dim;
   p.row_sH = c->stride_h / c->head_dim;
   p.row_sS = c->stride_s / c->head_dim;

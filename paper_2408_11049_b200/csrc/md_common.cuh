@@ -160,6 +160,12 @@ MD_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 }  // namespace md
 
 namespace md {
+// Touch a global address (one L2 load, result discarded) so its address translation is
+// resident before a latency-critical store / atomic to the same page.
+MD_DEV void touch_global(const void* ptr) {
+  uint32_t x;
+  asm volatile("ld.global.cg.b32 %0, [%1];" : "=r"(x) : "l"(ptr) : "memory");
+}
 MD_DEV uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -22,7 +22,7 @@ v = torch.empty_like(k)
 SC.fill_cache(k, 1, S.T_KCACHE, 0, cap)
 SC.fill_cache(v, 1, S.T_VCACHE, 0, cap)
 scale = float(np.float32(1 / np.sqrt(d)))
-trace = torch.zeros((1024, 8), dtype=torch.int64, device="cuda")
+trace = torch.zeros((1024, 16), dtype=torch.int64, device="cuda")
 if mode == "draft":
     q = torch.empty((B, Hq, d), dtype=torch.bfloat16, device="cuda")
     SC.fill_q(q, 1, S.T_QDRAFT, Hkv)
@@ -54,9 +54,13 @@ t = trace.cpu().numpy().astype(np.float64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 rel = (t - t0) / 1e3
-names = ["entry", "after_wait", "range_located", "first_tile", "last_epilogue", "end"]
+names = {0: "entry", 1: "after_wait", 2: "range_located", 3: "first_tile", 4: "last_epilogue", 5: "end",
+         7: "epi_combined", 8: "epi_stored", 9: "epi_merged", 10: "producer_done"}
 res = {"mode": mode, "window": window, "ctas": int(len(t)), "call_us_back_to_back": a.elapsed_time(b) / 20 * 1e3}
-for i, nme in enumerate(names):
+res["segments"] = [int(x) for x in np.percentile(t[:, 11], [0, 50, 100])]
+for i, nme in names.items():
+    if not np.all(t[:, i] > 0):
+        continue
     col = rel[:, i]
     res[nme] = [round(float(np.percentile(col, q)), 2) for q in (0, 10, 50, 90, 100)]
 res["span_end_minus_entry_p50"] = round(float(np.median(rel[:, 5] - rel[:, 0])), 2)
