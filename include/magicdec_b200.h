@@ -108,13 +108,15 @@ MD_API md_status md_kv_append(const md_kv_cache* cache, const void* k_new, const
                        const int32_t* start_pos, md_stream_t stream);
 
 /*
- * Bytes of scratch the attention calls need: per-CTA split partials
- * (o, lse) of the units that straddle two CTAs of the persistent stream-K grid, and one
- * arrival counter per (b, kv head).  Depends on (B, Hkv, g*T, head_dim) and the current
- * device's SM count, not on the context length (`max_kv_len` is accepted for symmetry).
+ * Bytes of scratch the attention calls need: a fixed block of arrival
+ * counters (one per (b, kv head), up to B*Hkv = 65536, plus two for the dynamic chunk
+ * scheduler) followed by the split partials (o, lse) of the work chunks of the persistent
+ * grid.  Depends on (g*T, head_dim) and the current device's SM count, not on the context
+ * length (`max_kv_len` and `batch` are accepted for symmetry).
  * The workspace must be zero-filled ONCE when allocated (e.g. cudaMemset / torch.zeros);
- * every call leaves the counters at zero again, so it can be reused by any later call on
- * the same stream (not by two calls in flight concurrently).  Returns 0 for invalid args.
+ * every call leaves the counters at zero again, so it can be reused by any later call of any
+ * shape on the same stream (not by two calls in flight concurrently).  Returns 0 for
+ * invalid args.
  */
 MD_API size_t md_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads, int32_t head_dim,
                                int32_t T, int32_t max_kv_len);

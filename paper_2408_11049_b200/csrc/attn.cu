@@ -68,7 +68,10 @@ struct AttnParams {
   int64_t row_sB, row_sH, row_sS;  // cache strides in units of rows (d elements), for gather4
   unsigned long long* trace;       // diagnostics: [G][8] globaltimer stamps (md_debug_trace), or null
   int fused_merge;        // 1: the last CTA of a split unit merges (acq_rel counter); 0: attn_merge_kernel
-  int warm;               // producer lanes touch each segment's output / workspace / counter early
+  int* dyn;               // [2] dynamic chunk counter and finished-CTA counter (zero between calls)
+  int dyn_k;              // dynamic chunks per active CTA (0: static stream-K only)
+  int dyn_static_permille;  // share of the tiles assigned statically (per mille)
+  int dyn_min_tiles;      // dynamic only when total tiles >= dyn_min_tiles * active CTAs
   const uint32_t* tree_mask;  // verify: [B][T] bit j of (b, t) = node t sees new key n-T+j (null: causal chain)
   int mode;
   float scale_log2;       // scale * log2(e)
@@ -132,13 +135,45 @@ __device__ int64_t total_tiles(const AttnParams& p, const int* pre) {
 __device__ __forceinline__ int tiles_of(const AttnParams& p, const int* pre, int b) {
   return p.B <= TABLE_B ? (pre[b + 1] - pre[b]) / p.Hkv : unit_tiles(p, b);
 }
-// The active grid is G = min(gridDim.x, total) so that every active CTA owns >= 1 tile
-// (an empty CTA would never arrive on a unit's counter); CTAs >= G exit at once.
-__device__ __forceinline__ int active_ctas(int64_t total) { return total < (int64_t)gridDim.x ? static_cast<int>(total) : (int)gridDim.x; }
-__device__ __forceinline__ int64_t cta_start(int c, int64_t total, int G) { return (int64_t)c * total / G; }
-// the CTA whose range holds global tile t: largest c with cta_start(c) <= t
-__device__ __forceinline__ int cta_of(int64_t t, int64_t total, int G) {
-  return static_cast<int>(((t + 1) * G + total - 1) / total - 1);
+// Work plan over the global tile space [0, total).  Chunks 0..G-1 are static: equal
+// contiguous ranges covering [0, S0), chunk c processed by CTA c.  If dynamic balancing is on,
+// chunks G..nch-1 of CH tiles cover [S0, total) and are claimed at run time from an atomic
+// counter by whichever CTA's producer runs out of work first (per-SM HBM bandwidth differs
+// by several percent, so equal static shares finish at different times).  Every chunk is
+// non-empty (S0 >= G, and G = min(gridDim.x, total): an empty chunk would never arrive on a
+// unit's counter); CTAs >= G exit at once.  A split unit's partials live in the slots of
+// the chunks covering it: chunk * 2 + (0 if the unit is the chunk's first, 1 if its last).
+struct Plan {
+  int64_t total, S0, CH;
+  int G, nch;
+  __device__ int64_t start(int c) const {
+    return c <= G ? (int64_t)c * S0 / G : min(total, S0 + (int64_t)(c - G) * CH);
+  }
+  // the chunk holding global tile t: largest c with start(c) <= t
+  __device__ int chunk_of(int64_t t) const {
+    return t < S0 ? static_cast<int>(((t + 1) * G + S0 - 1) / S0 - 1) : G + static_cast<int>((t - S0) / CH);
+  }
+  __device__ int slot(int64_t ustart, int c) const { return ustart > start(c) ? 1 : 0; }
+};
+__device__ Plan make_plan(const AttnParams& p, int64_t total, int grid) {
+  Plan pl;
+  pl.total = total;
+  pl.G = total < (int64_t)grid ? static_cast<int>(total) : grid;
+  pl.S0 = total;
+  pl.CH = 1;
+  pl.nch = pl.G;
+  // short calls (few tiles per CTA, e.g. every draft call) stay static: extra segments and
+  // hand-offs cost more there than the bandwidth imbalance they remove
+  if (p.dyn_k > 0 && total >= (int64_t)p.dyn_min_tiles * pl.G) {
+    const int64_t S0 = max((int64_t)pl.G, total * p.dyn_static_permille / 1000);
+    if (S0 < total) {
+      const int64_t rest = total - S0, per = (int64_t)pl.G * p.dyn_k;
+      pl.S0 = S0;
+      pl.CH = (rest + per - 1) / per;
+      pl.nch = pl.G + static_cast<int>((rest + pl.CH - 1) / pl.CH);  // <= G * (1 + dyn_k)
+    }
+  }
+  return pl;
 }
 
 // One contiguous piece of one unit processed by one CTA: tiles [lo, hi) of `tiles`.
@@ -235,10 +270,6 @@ __device__ __forceinline__ Ranges seg_ranges(const AttnParams& p, const Seg& sg)
   return r;
 }
 
-// The partial slot of CTA c for a unit starting at ustart: 0 if it is c's first unit, 1 if its last.
-__device__ __forceinline__ int slot_of(int64_t ustart, int c, int64_t total, int G) {
-  return ustart > cta_start(c, total, G) ? 1 : 0;
-}
 
 // diagnostics: consumer warp 0 / lane 0 stamps phase k of this CTA (md_debug_trace)
 constexpr int TRACE_SLOTS = 16;
@@ -338,44 +369,44 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
 // partial stores before thread 0's release-add; the acq_rel atomic of the last arriver
 // makes all contributors' stores visible to its CTA (read back with ld.global.cg).
 template <int D>
-__device__ void finish_unit(const AttnParams& p, const Seg& sg, int64_t total, int nthr, int* flag) {
-  const int G = active_ctas(total);
+__device__ void finish_unit(const AttnParams& p, const Seg& sg, const Plan& pl, int nthr, int* flag) {
   named_bar_sync(1, nthr);
   if (threadIdx.x == 0) {
-    const int cf = cta_of(sg.ustart, total, G), cl = cta_of(sg.ustart + sg.tiles - 1, total, G);
+    const int cf = pl.chunk_of(sg.ustart), cl = pl.chunk_of(sg.ustart + sg.tiles - 1);
     const int old = atomic_add_acq_rel_gpu(p.counters + sg.unit, 1);
     const int last = (old == cl - cf);
     if (last) p.counters[sg.unit] = 0;  // leave the workspace ready for the next call
     flag[0] = last;
     flag[1] = cf;
     flag[2] = cl;
-    // the unit is the LAST segment of CTA cf iff cf's range began before it (slot 1); for
-    // every later CTA it is the first segment (slot 0)
-    flag[3] = slot_of(sg.ustart, cf, total, G);
+    // the unit is the LAST segment of chunk cf iff cf began before it (slot 1); for every
+    // later chunk it is the first segment (slot 0)
+    flag[3] = pl.slot(sg.ustart, cf);
   }
   named_bar_sync(1, nthr);
   if (!flag[0]) return;
   const int cf = flag[1], cl = flag[2], s0 = flag[3];
+  // each thread owns (row, 4 columns) elements; every partial's lse and values are loaded
+  // together and combined online, so the merge costs one L2 round trip per partial
   constexpr int V4 = D / 4;
   for (int idx = threadIdx.x; idx < p.R * V4; idx += nthr) {
     const int r = idx / V4, c4 = (idx - r * V4) * 4;
-    float M = -INFINITY;
-#pragma unroll 4
-    for (int c = cf; c <= cl; ++c)
-      M = fmaxf(M, __ldcg(p.ws_lse + ((int64_t)c * 2 + (c == cf ? s0 : 0)) * p.R + r));
-    float W = 0.f;
+    float M = -INFINITY, W = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
+#pragma unroll 2
     for (int c = cf; c <= cl; ++c) {
       const int64_t prow = ((int64_t)c * 2 + (c == cf ? s0 : 0)) * p.R + r;
       const float ls = __ldcg(p.ws_lse + prow);
       const float4 v = __ldcg(reinterpret_cast<const float4*>(p.ws_o + prow * D + c4));
-      const float w = (ls == -INFINITY) ? 0.f : ex2(ls - M);  // empty partials hold finite zeros
-      W += w;
-      acc.x += w * v.x;
-      acc.y += w * v.y;
-      acc.z += w * v.z;
-      acc.w += w * v.w;
+      if (ls == -INFINITY) continue;  // an empty partial
+      const float mn = fmaxf(M, ls);
+      const float a = ex2(M - mn), w = ex2(ls - mn);  // a = 0 on the first partial
+      M = mn;
+      W = W * a + w;
+      acc.x = acc.x * a + w * v.x;
+      acc.y = acc.y * a + w * v.y;
+      acc.z = acc.z * a + w * v.z;
+      acc.w = acc.w * a + w * v.w;
     }
     const float inv = W > 0.f ? 1.f / W : 0.f;
     const int64_t orow = out_row(p, sg.b, sg.kvh, r);
@@ -394,7 +425,7 @@ __global__ void __launch_bounds__(128) attn_merge_kernel(const AttnParams p, int
   build_prefix(p, pre);
   const int64_t total = total_tiles(p, pre);
   if (total == 0) return;
-  const int G = total < (int64_t)grid_attn ? static_cast<int>(total) : grid_attn;
+  const Plan pl = make_plan(p, total, grid_attn);
   const int unit = blockIdx.x, b = unit / p.Hkv, kvh = unit - b * p.Hkv;
   int64_t bstart = 0;
   if (p.B <= TABLE_B) {
@@ -405,17 +436,17 @@ __global__ void __launch_bounds__(128) attn_merge_kernel(const AttnParams p, int
   const int tiles = tiles_of(p, pre, b);
   if (tiles == 0) return;
   const int64_t ustart = bstart + (int64_t)kvh * tiles;
-  const int cf = cta_of(ustart, total, G), cl = cta_of(ustart + tiles - 1, total, G);
-  if (cf == cl) return;  // written whole by one CTA
+  const int cf = pl.chunk_of(ustart), cl = pl.chunk_of(ustart + tiles - 1);
+  if (cf == cl) return;  // written whole by one chunk
   constexpr int V4 = D / 4;
   for (int idx = threadIdx.x; idx < p.R * V4; idx += blockDim.x) {
     const int r = idx / V4, c4 = (idx - r * V4) * 4;
     float M = -INFINITY;
-    for (int c = cf; c <= cl; ++c) M = fmaxf(M, p.ws_lse[((int64_t)c * 2 + slot_of(ustart, c, total, G)) * p.R + r]);
+    for (int c = cf; c <= cl; ++c) M = fmaxf(M, p.ws_lse[((int64_t)c * 2 + pl.slot(ustart, c)) * p.R + r]);
     float W = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int c = cf; c <= cl; ++c) {
-      const int64_t prow = ((int64_t)c * 2 + slot_of(ustart, c, total, G)) * p.R + r;
+      const int64_t prow = ((int64_t)c * 2 + pl.slot(ustart, c)) * p.R + r;
       const float ls = p.ws_lse[prow];
       if (ls == -INFINITY) continue;
       const float w = ex2(ls - M);
@@ -489,12 +520,10 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
   trace_stamp(p, 1);
   __syncthreads();
   build_prefix(p, pre);
-  const int64_t total = total_tiles(p, pre);
-  const int G = active_ctas(total);
-  if ((int)blockIdx.x >= G) return;  // uniform across the CTA
-  const int64_t S = cta_start(blockIdx.x, total, G), E = cta_start(blockIdx.x + 1, total, G);
+  const Plan pl = make_plan(p, total_tiles(p, pre), gridDim.x);  // static: the host sets dyn_k = 0
+  if ((int)blockIdx.x >= pl.G) return;  // uniform across the CTA
   SegWalker walk;
-  walk.init(p, pre, S, E);
+  walk.init(p, pre, pl.start(blockIdx.x), pl.start(blockIdx.x + 1));
   Seg sg;
   trace_stamp(p, 2);
 
@@ -715,7 +744,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
     named_bar_sync(1, NC * 32);
     // sum the KS slices and store rows r < R (final output, or this CTA's partial slot)
     const bool complete = sg.complete();
-    const int slot_base = blockIdx.x * 2 + slot_of(sg.ustart, blockIdx.x, total, G);
+    const int slot_base = blockIdx.x * 2 + pl.slot(sg.ustart, blockIdx.x);
     constexpr int V4 = D / 4;
     for (int idx = threadIdx.x; idx < p.R * V4; idx += NC * 32) {
       const int r = idx / V4, c4 = (idx - r * V4) * 4;
@@ -740,7 +769,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
         if (c4 == 0) __stcg(p.ws_lse + prow, lse2);
       }
     }
-    if (!complete && p.fused_merge) finish_unit<D>(p, sg, total, NC * 32, flag);
+    if (!complete && p.fused_merge) finish_unit<D>(p, sg, pl, NC * 32, flag);
     fence_proxy_async();         // order our generic writes to the ring before later TMA writes
     named_bar_sync(1, NC * 32);  // the scratch (= ring) may now be refilled
     if (lane == 0) mbar_arrive(epi_done);
@@ -757,7 +786,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
 template <int D, int KS, int CTAS>
 struct KeysCfg {
   static constexpr int NC = KS;
-  static constexpr int THREADS = (NC + 1) * 32;
+  static constexpr int THREADS = (NC + 1) * 32;  // + TMA producer warp
   static constexpr int KW = TK / KS;       // keys per consumer warp per tile
   static constexpr int KB = KW / 16;       // 16-key blocks per warp per tile
   static constexpr int ROWS = 8;           // query rows (padded)
@@ -767,7 +796,7 @@ struct KeysCfg {
   static constexpr int QBUF = 2 * ROWS * QSTR;
   static constexpr int FRAG = (D / 16) * 4 * 32;  // fp32 of one warp's O^T fragments
   static constexpr int EPI = (NC / 2) * FRAG * 4 + NC * ROWS * 2 * 4 + ROWS * 4 + 64;
-  static constexpr int FIXED = QBUF + EPI + 256 /*barriers*/ + TABLE_BYTES + 1024 /*alignment slack*/;
+  static constexpr int FIXED = QBUF + EPI + 256 /*barriers, hand-off slots*/ + TABLE_BYTES + 1024 /*alignment slack*/;
   static constexpr int NSTAGE_FIT = ((CTAS == 1 ? 227 * 1024 : 112 * 1024) - FIXED) / STAGE;
   static constexpr int NSTAGE = NSTAGE_FIT > 8 ? 8 : NSTAGE_FIT;
   static constexpr int SMEM = NSTAGE * STAGE + FIXED;
@@ -791,12 +820,15 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   float* obuf = reinterpret_cast<float*>(qbuf + C::QBUF);  // [NC/2][FRAG]    O^T fragments (tree merge)
   float* mlbuf = obuf + (NC / 2) * FRAG;                    // [NC][8][2]      (m, l) per warp row
   float* lsebuf = mlbuf + NC * C::ROWS * 2;                 // [8]             combined lse (log2)
-  int* flag = reinterpret_cast<int*>(lsebuf + C::ROWS);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(obuf) + C::EPI);
   uint64_t* empty = full + NSTAGE;
   uint64_t* qfull = empty + NSTAGE;
   uint64_t* qempty = qfull + 2;
-  int* pre = reinterpret_cast<int*>(qempty + 2);  // [TABLE_B + 1] per-sequence tile prefix
+  uint64_t* cfull = qempty + 2;   // dynamic chunk hand-off, producer -> consumers (2 slots)
+  uint64_t* cempty = cfull + 2;
+  int* cids = reinterpret_cast<int*>(cempty + 2);
+  int* flag = cids + 2;  // [4] finish_unit
+  int* pre = flag + 4;  // [TABLE_B + 1] per-sequence tile prefix
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -807,6 +839,8 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&qfull[s], 1);
       mbar_init(&qempty[s], NC);
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], NC);
     }
     fence_mbar_init();
   }
@@ -821,12 +855,11 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   trace_stamp(p, 1);
   __syncthreads();
   build_prefix(p, pre);
-  const int64_t total = total_tiles(p, pre);
-  const int G = active_ctas(total);
-  if ((int)blockIdx.x >= G) return;  // uniform across the CTA
-  const int64_t S = cta_start(blockIdx.x, total, G), E = cta_start(blockIdx.x + 1, total, G);
+  const Plan pl = make_plan(p, total_tiles(p, pre), gridDim.x);
+  if ((int)blockIdx.x >= pl.G) return;  // uniform across the CTA
+  int chunk = blockIdx.x;                // this CTA's static chunk, then claimed dynamic ones
   SegWalker walk;
-  walk.init(p, pre, S, E);
+  walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
   Seg sg;
   trace_stamp(p, 2);
 
@@ -843,8 +876,34 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       }
     }
     const uint64_t pol = policy_evict_first();
-    int it = 0, qi = 0;
-    while (walk.next(p, sg)) {
+    int it = 0, qi = 0, ck = 0;
+    // Dynamic chunks are claimed one ahead (the atomic's latency hides behind a whole chunk
+    // of TMA issue); when the current chunk is exhausted the claimed id (-1: none left) is
+    // handed to the consumers.
+    int ahead = 0;
+    if (pl.nch > pl.G && lane == 0) ahead = atomicAdd(p.dyn, 1);
+    auto next_seg = [&]() -> bool {
+      while (!walk.next(p, sg)) {
+        if (pl.nch == pl.G) return false;
+        int nxt = -1;
+        if (lane == 0) {
+          const int c = pl.G + ahead;
+          nxt = c < pl.nch ? c : -1;
+          if (nxt >= 0) ahead = atomicAdd(p.dyn, 1);
+          const int cs = ck & 1;
+          mbar_wait(&cempty[cs], ((ck >> 1) & 1) ^ 1);
+          cids[cs] = nxt;
+          mbar_arrive(&cfull[cs]);
+        }
+        nxt = __shfl_sync(0xffffffffu, nxt, 0);
+        ++ck;
+        if (nxt < 0) return false;
+        chunk = nxt;
+        walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+      }
+      return true;
+    };
+    while (next_seg()) {
       // this segment's query rows: row r = (t = r / g, head = kvh*g + r % g)
       if (lane == 0) {
         const int qs = qi & 1;
@@ -852,10 +911,6 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         mbar_arrive_expect_tx(&qfull[qs], p.R * D * 2);
         for (int r = 0; r < p.R; ++r)
           bulk_load(qbuf + (qs * C::ROWS + r) * C::QSTR, p.q + out_row(p, sg.b, sg.kvh, r) * D, D * 2, &qfull[qs]);
-      } else if (p.warm && lane < 4) {
-        if (lane == 1) touch_global(p.out + out_row(p, sg.b, sg.kvh, 0) * D);
-        if (lane == 2) touch_global(p.ws_o + (int64_t)blockIdx.x * 2 * p.R * D);
-        if (lane == 3) touch_global(p.counters + sg.unit);
       }
       __syncwarp();
       produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol);
@@ -864,15 +919,29 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     if (lane == 0) trace_put(p, 10, globaltimer());
     return;
   }
-
   // ============================== consumers ==============================
   const int ks = warp;
   const int gq = lane >> 2, cq = lane & 3;  // fragment row group / column quad
   const uint32_t ring = smem_u32(smem);
   const uint32_t qring = smem_u32(qbuf);
-  int it = 0, qi = 0;
+  int it = 0, qi = 0, ck = 0;
   unsigned long long qi_seg = 0;
-  while (walk.next(p, sg)) {
+  auto next_seg = [&]() -> bool {  // mirrors the producer's chunk sequence
+    while (!walk.next(p, sg)) {
+      if (pl.nch == pl.G) return false;
+      const int cs = ck & 1;
+      mbar_wait(&cfull[cs], (ck >> 1) & 1);
+      const int nxt = cids[cs];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cempty[cs]);
+      ++ck;
+      if (nxt < 0) return false;
+      chunk = nxt;
+      walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+    }
+    return true;
+  };
+  while (next_seg()) {
     const int n = sg.n;
     const Ranges rg = seg_ranges(p, sg);
     // new-key visibility of the two rows 2cq, 2cq+1 this thread holds (verify; rows past R
@@ -1076,7 +1145,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     trace_stamp(p, 7);
     // rows r < R -> the final output, or this CTA's partial slot
     const bool complete = sg.complete();
-    const int slot_base = blockIdx.x * 2 + slot_of(sg.ustart, blockIdx.x, total, G);
+    const int slot_base = chunk * 2 + pl.slot(sg.ustart, chunk);
     {
       constexpr int V4 = D / 4;
       for (int idx = threadIdx.x; idx < p.R * V4; idx += NC * 32) {
@@ -1097,12 +1166,20 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       }
     }
     trace_stamp(p, 8);
-    if (!complete && p.fused_merge) finish_unit<D>(p, sg, total, NC * 32, flag);
+    if (!complete && p.fused_merge) finish_unit<D>(p, sg, pl, NC * 32, flag);
     trace_stamp(p, 9);
     named_bar_sync(1, NC * 32);  // the epilogue buffers are reused by the next segment
     trace_stamp(p, 5);
     ++qi_seg;
     if (threadIdx.x == 0) trace_put(p, 11, qi_seg);
+  }
+  // the last CTA to finish re-arms the dynamic counters for the next call (every CTA's
+  // producer has made its final claim before its consumers saw the -1 hand-off)
+  if (pl.nch > pl.G && threadIdx.x == 0) {
+    if (atomicAdd(p.dyn + 1, 1) == pl.G - 1) {
+      p.dyn[0] = 0;
+      p.dyn[1] = 0;
+    }
   }
 }
 
@@ -1142,9 +1219,31 @@ static int grid_for(int R, int sm_count) {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// [partials fp32 G*2*R*D][partial lse fp32 G*2*R][counters int32 B*Hkv]
+// Dynamic chunks per active CTA (keys kernel only; the rows kernel's epilogue aliases its
+// ring, so extra segment boundaries would stall its producer): MD_DYN_K, default 4.
+static int dyn_k_for(int R) {
+  static const int k = env_int("MD_DYN_K", 4);
+  return use_keys_kernel(R) ? (k < 0 ? 0 : k) : 0;
+}
+static int dyn_min_tiles() {  // 128 tiles = 8 MB of K+V per CTA at d = 128 (MD_DYN_MIN)
+  static const int v = env_int("MD_DYN_MIN", 128);
+  return v < 1 ? 1 : v;
+}
+static int dyn_static_permille() {
+  static const int v = env_int("MD_DYN_STATIC", 750);
+  return v < 0 ? 0 : (v > 1000 ? 1000 : v);
+}
+
+// [counters int32: 2 dynamic-chunk counters + MAX_UNITS unit counters][partials fp32 C*2*R*D]
+// [partial lse fp32 C*2*R], C = G*(1+dyn_k) chunks (G static + at most G*dyn_k dynamic).
+// The counters sit at a fixed offset with a fixed capacity, so calls of ANY shape can share
+// one workspace: no call's partials ever overlap another call's counters.
+constexpr int MAX_UNITS = 65536;  // B * Hkv
+constexpr size_t COUNTER_BYTES = ((size_t)(MAX_UNITS + 2) * 4 + 255) & ~size_t(255);
 static size_t workspace_for(int G, int units, int R, int D) {
-  return align256((size_t)G * 2 * R * D * 4) + align256((size_t)G * 2 * R * 4) + align256((size_t)units * 4);
+  (void)units;
+  const size_t C = (size_t)G * (1 + dyn_k_for(R));
+  return COUNTER_BYTES + align256(C * 2 * R * D * 4) + align256(C * 2 * R * 4);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -1277,6 +1376,8 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   const int R = g * T;
   MD_REQUIRE(R <= 64, MD_ERR_UNSUPPORTED, "%s: g*T = %d > 64 query rows per KV head is not supported", who, R);
   const int units = c->batch * c->num_kv_heads;
+  MD_REQUIRE(units <= MAX_UNITS, MD_ERR_UNSUPPORTED, "%s: batch * num_kv_heads = %d > %d is not supported", who,
+             units, MAX_UNITS);
   const int grid = grid_for(R, device_sm_count());
   const size_t need = workspace_for(grid, units, R, c->head_dim);
   MD_REQUIRE(ws != nullptr && ws_bytes >= need, MD_ERR_WORKSPACE, "%s: workspace of %zu bytes required, %zu given",
@@ -1318,16 +1419,20 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.tree_mask = ix.tree_mask;
   p.trace = (g_trace != nullptr && g_trace_bytes >= (size_t)grid * TRACE_SLOTS * 8) ? g_trace : nullptr;
   p.fused_merge = fused_merge_enabled();
-  p.warm = env_int("MD_WARM", 1);
   p.row_sB = c->stride_b / c->head_dim;
   p.row_sH = c->stride_h / c->head_dim;
   p.row_sS = c->stride_s / c->head_dim;
+  p.dyn_k = dyn_k_for(R);
+  p.dyn_static_permille = dyn_static_permille();
+  p.dyn_min_tiles = dyn_min_tiles();
+  const size_t chunks = (size_t)grid * (1 + p.dyn_k);
   uint8_t* w = static_cast<uint8_t*>(ws);
+  p.dyn = reinterpret_cast<int*>(w);
+  p.counters = p.dyn + 2;
+  w += COUNTER_BYTES;
   p.ws_o = reinterpret_cast<float*>(w);
-  w += align256((size_t)grid * 2 * R * c->head_dim * 4);
+  w += align256(chunks * 2 * R * c->head_dim * 4);
   p.ws_lse = reinterpret_cast<float*>(w);
-  w += align256((size_t)grid * 2 * R * 4);
-  p.counters = reinterpret_cast<int*>(w);
   st = (c->head_dim == 128) ? launch_dim<128>(tm, p, grid, s) : launch_dim<64>(tm, p, grid, s);
   if (st != MD_OK || p.fused_merge) return st;
   if (c->head_dim == 128)
