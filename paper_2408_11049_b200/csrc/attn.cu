@@ -51,12 +51,14 @@ struct TmapSet {
   CUtensorMap k_full, v_full, k_part, v_part, k_rows, v_rows;
 };
 
+constexpr int XS_FRAGS = 3;  // rows kernel: at most MT * (KS - 1) = 3 parked warp fragments per CTA
+
 struct AttnParams {
   const uint16_t* q;      // bf16 [B][T][Hq][D]
   float* out;             // [B][T][Hq][D]
   float* lse;             // [B][T][Hq] natural log, may be null
-  float* ws_o;            // [G][2][R][D] normalised partial outputs
-  float* ws_lse;          // [G][2][R]    partial lse, log2 units (-inf if empty)
+  float* ws_o;            // [chunks][2][R][D] normalised partial outputs
+  float* ws_lse;          // [chunks][2][R]    partial lse, log2 units (-inf if empty)
   int* counters;          // [B*Hkv] arrival counters (zero between calls)
   const int32_t* kv_len;  // [B]
   int B, Hq, Hkv, T, g, R;
@@ -69,6 +71,7 @@ struct AttnParams {
   unsigned long long* trace;       // diagnostics: [G][8] globaltimer stamps (md_debug_trace), or null
   int fused_merge;        // 1: the last CTA of a split unit merges (acq_rel counter); 0: attn_merge_kernel
   int* dyn;               // [2] dynamic chunk counter and finished-CTA counter (zero between calls)
+  float* ws_x;            // rows kernel: per-CTA [XS_FRAGS][16][D] fragment scratch (key-slice sum)
   int dyn_k;              // dynamic chunks per active CTA (0: static stream-K only)
   int dyn_static_permille;  // share of the tiles assigned statically (per mille)
   int dyn_min_tiles;      // dynamic only when total tiles >= dyn_min_tiles * active CTAs
@@ -188,9 +191,7 @@ struct Seg {
 struct SegWalker {
   int64_t t, end, ustart;
   int b, h, tiles_b;
-  const int* pre;
-  __device__ void init(const AttnParams& p, const int* pre_, int64_t S, int64_t E) {
-    pre = pre_;
+  __device__ void init(const AttnParams& p, const int* pre, int64_t S, int64_t E) {
     t = S;
     end = E;
     int64_t acc = 0;
@@ -218,7 +219,7 @@ struct SegWalker {
     h = static_cast<int>((S - acc) / tiles_b);
     ustart = acc + (int64_t)h * tiles_b;
   }
-  __device__ bool next(const AttnParams& p, Seg& sg) {
+  __device__ bool next(const AttnParams& p, const int* pre, Seg& sg) {
     if (t >= end) return false;
     sg.b = b;
     sg.kvh = h;
@@ -467,16 +468,18 @@ __global__ void __launch_bounds__(128) attn_merge_kernel(const AttnParams p, int
 // ============================================================================ rows kernel
 // Query rows on the MMA M dimension.  Consumer warp (mt, ks) owns query-row tile mt (16 of
 // the R rows) and the ks-th KW-key slice of every 64-key tile: S = Q K^T, O += P V.
-// 2 CTAs / SM; the epilogue scratch aliases the ring, so at a segment boundary the producer
-// waits for the consumers' epilogue (epi_done) before refilling — at most ~2 boundaries
-// per CTA under stream-K.
+// 2 CTAs / SM.  The key-slice sum of the epilogue goes through a per-CTA scratch in the
+// workspace (L2-resident), so the ring is never aliased and the producer streams straight
+// across segment boundaries (and dynamic chunks).
 template <int D>
 struct RowsSmem {
   static constexpr int NSTAGE = 3;  // 3 x 32 KB at d=128 -> 2 CTAs / SM
   static constexpr int TILE_BYTES = TK * D * 2;
   static constexpr int STAGE_BYTES = 2 * TILE_BYTES;
   static constexpr int RING_BYTES = NSTAGE * STAGE_BYTES;
-  static constexpr int TOTAL = RING_BYTES + 1024 /*align slack*/ + (2 * NSTAGE + 1) * 8 + 64 + TABLE_BYTES;
+  static constexpr int EPI_BYTES = 4 * 16 * 2 * 4 + 4 * 16 * 4;  // mlbuf [NC<=4][16][2] + lsebuf [MT<=4][16]
+  static constexpr int TOTAL = RING_BYTES + 1024 /*align slack*/ + (2 * NSTAGE + 4) * 8 + 16 /*cids*/ + 128 /*flag, plan*/ +
+                               EPI_BYTES + TABLE_BYTES;
 };
 
 // 2 CTAs / SM (ptxas then keeps <= 3 warps' registers per SM sub-partition: 168 regs at 5 warps).
@@ -488,12 +491,10 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
   constexpr int NT_S = KW / 8; // n8 tiles of S per warp
   constexpr int NT_O = D / 8;  // n8 tiles of O
   constexpr int KQ = D / 16;   // k16 steps of QK^T
-  constexpr int OSTR = D + 4;  // padded fp32 row stride of the merge buffer
   using L = RowsSmem<D>;
   constexpr int NSTAGE = L::NSTAGE;
   static_assert(KW % 16 == 0, "key slice must be a multiple of 16");
-  static_assert(NC * 16 * OSTR * 4 + NC * 16 * 2 * 4 + MT * 16 * 4 <= L::RING_BYTES,
-                "epilogue buffer must fit in the ring");
+  static_assert(NC <= 4 && MT <= 4 && MT * (KS - 1) <= XS_FRAGS, "epilogue buffers are sized for <= 4 warps");
 
   extern __shared__ uint8_t smem_raw[];
   // align to 1 KB by offsetting the __shared__ array itself, so every derived pointer keeps
@@ -501,9 +502,14 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::RING_BYTES);
   uint64_t* empty = full + NSTAGE;
-  uint64_t* epi_done = empty + NSTAGE;
-  int* flag = reinterpret_cast<int*>(epi_done + 1);
-  int* pre = flag + 16;  // [TABLE_B + 1] per-sequence tile prefix
+  uint64_t* cfull = empty + NSTAGE;  // dynamic chunk hand-off, producer -> consumers (2 slots)
+  uint64_t* cempty = cfull + 2;
+  int* cids = reinterpret_cast<int*>(cempty + 2);
+  int* flag = cids + 4;                                   // [16] finish_unit
+  Plan* plan_smem = reinterpret_cast<Plan*>(flag + 16);   // 40 bytes (reserved 64)
+  float* mlbuf = reinterpret_cast<float*>(flag + 32);     // [NC][16][2] (m, l) per warp row
+  float* lsebuf = mlbuf + 4 * 16 * 2;                     // [MT*16] combined lse (log2)
+  int* pre = reinterpret_cast<int*>(lsebuf + 4 * 16);     // [TABLE_B + 1] per-sequence tile prefix
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -511,7 +517,10 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NC);
     }
-    mbar_init(epi_done, NC);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], NC);
+    }
     fence_mbar_init();
   }
   trace_stamp(p, 0);
@@ -520,10 +529,14 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
   trace_stamp(p, 1);
   __syncthreads();
   build_prefix(p, pre);
-  const Plan pl = make_plan(p, total_tiles(p, pre), gridDim.x);  // static: the host sets dyn_k = 0
+  // the plan lives in shared memory (read only at segment boundaries: keeps registers free)
+  if (threadIdx.x == 0) *plan_smem = make_plan(p, total_tiles(p, pre), gridDim.x);
+  __syncthreads();
+  const Plan& pl = *plan_smem;
   if ((int)blockIdx.x >= pl.G) return;  // uniform across the CTA
+  int chunk = blockIdx.x;                // this CTA's static chunk, then claimed dynamic ones
   SegWalker walk;
-  walk.init(p, pre, pl.start(blockIdx.x), pl.start(blockIdx.x + 1));
+  walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
   Seg sg;
   trace_stamp(p, 2);
 
@@ -540,15 +553,32 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
       }
     }
     const uint64_t pol = policy_evict_first();
-    int it = 0, si = 0;
-    while (walk.next(p, sg)) {
-      if (si > 0) {  // the ring doubles as epilogue scratch
-        if (lane == 0) mbar_wait(epi_done, (si - 1) & 1);
-        __syncwarp();
+    int it = 0, ck = 0;
+    int ahead = 0;  // dynamic chunk claimed one ahead (see the keys kernel)
+    if (pl.nch > pl.G && lane == 0) ahead = atomicAdd(p.dyn, 1);
+    auto next_seg = [&]() -> bool {
+      while (!walk.next(p, pre, sg)) {
+        if (pl.nch == pl.G) return false;
+        int nxt = -1;
+        if (lane == 0) {
+          const int c = pl.G + ahead;
+          nxt = c < pl.nch ? c : -1;
+          if (nxt >= 0) ahead = atomicAdd(p.dyn, 1);
+          const int cs = ck & 1;
+          mbar_wait(&cempty[cs], ((ck >> 1) & 1) ^ 1);
+          cids[cs] = nxt;
+          mbar_arrive(&cfull[cs]);
+        }
+        nxt = __shfl_sync(0xffffffffu, nxt, 0);
+        ++ck;
+        if (nxt < 0) return false;
+        chunk = nxt;
+        walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
       }
+      return true;
+    };
+    while (next_seg())
       produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol);
-      ++si;
-    }
     return;
   }
 
@@ -556,11 +586,23 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
   const int mt = warp / KS, ks = warp - mt * KS;
   const int gq = lane >> 2, cq = lane & 3;  // fragment row group / column quad
   const uint32_t ring = smem_u32(smem);
-  float* obuf = reinterpret_cast<float*>(smem);  // [NC][16][OSTR]   (aliases the ring)
-  float* mlbuf = obuf + NC * 16 * OSTR;           // [NC][16][2]
-  float* lsebuf = mlbuf + NC * 16 * 2;            // [MT*16]
-  int it = 0;
-  while (walk.next(p, sg)) {
+  int it = 0, ck = 0;
+  auto next_seg = [&]() -> bool {  // mirrors the producer's chunk sequence
+    while (!walk.next(p, pre, sg)) {
+      if (pl.nch == pl.G) return false;
+      const int cs = ck & 1;
+      mbar_wait(&cfull[cs], (ck >> 1) & 1);
+      const int nxt = cids[cs];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cempty[cs]);
+      ++ck;
+      if (nxt < 0) return false;
+      chunk = nxt;
+      walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+    }
+    return true;
+  };
+  while (next_seg()) {
     const int b = sg.b, kvh = sg.kvh, n = sg.n;
     const Ranges rg = seg_ranges(p, sg);
     // Q fragments for rows mt*16 + {gq, gq+8}; row r -> (t = r / g, head = kvh*g + r % g)
@@ -699,12 +741,12 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
     }
 
     // ============================== segment epilogue ==============================
+    // The ring is not touched: the producer keeps streaming the next segment meanwhile.
     trace_stamp(p, 4);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-    named_bar_sync(1, NC * 32);  // every consumer is done reading the ring
     if (cq == 0) {
       mlbuf[(warp * 16 + gq) * 2 + 0] = m0;
       mlbuf[(warp * 16 + gq) * 2 + 1] = l0;
@@ -713,6 +755,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
     }
     named_bar_sync(1, NC * 32);
     // scale this warp's O by 2^(m_w - M) / L where (M, L) combine the KS key slices
+    float f0, f1;
     {
       float M0 = -INFINITY, M1 = -INFINITY;
 #pragma unroll
@@ -728,52 +771,79 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
         if (e0[1] > 0.f) L0 += e0[1] * ex2(e0[0] - M0);
         if (e1[1] > 0.f) L1 += e1[1] * ex2(e1[0] - M1);
       }
-      const float f0 = (l0 > 0.f) ? ex2(m0 - M0) / L0 : 0.f;
-      const float f1 = (l1 > 0.f) ? ex2(m1 - M1) / L1 : 0.f;
+      f0 = (l0 > 0.f) ? ex2(m0 - M0) / L0 : 0.f;
+      f1 = (l1 > 0.f) ? ex2(m1 - M1) / L1 : 0.f;
       if (ks == 0 && cq == 0) {
         lsebuf[mt * 16 + gq] = (L0 > 0.f) ? M0 + __log2f(L0) : -INFINITY;
         lsebuf[mt * 16 + gq + 8] = (L1 > 0.f) ? M1 + __log2f(L1) : -INFINITY;
       }
-#pragma unroll
-      for (int i = 0; i < NT_O; ++i) {
-        const int d0 = i * 8 + cq * 2;
-        *reinterpret_cast<float2*>(&obuf[(warp * 16 + gq) * OSTR + d0]) = make_float2(o[i][0] * f0, o[i][1] * f0);
-        *reinterpret_cast<float2*>(&obuf[(warp * 16 + gq + 8) * OSTR + d0]) = make_float2(o[i][2] * f1, o[i][3] * f1);
-      }
     }
-    named_bar_sync(1, NC * 32);
-    // sum the KS slices and store rows r < R (final output, or this CTA's partial slot)
-    const bool complete = sg.complete();
-    const int slot_base = blockIdx.x * 2 + pl.slot(sg.ustart, blockIdx.x);
-    constexpr int V4 = D / 4;
-    for (int idx = threadIdx.x; idx < p.R * V4; idx += NC * 32) {
-      const int r = idx / V4, c4 = (idx - r * V4) * 4;
-      const int mtile = r >> 4, rin = r & 15;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int k = 0; k < KS; ++k) {
-        const float4 v = *reinterpret_cast<const float4*>(&obuf[((mtile * KS + k) * 16 + rin) * OSTR + c4]);
-        acc.x += v.x;
-        acc.y += v.y;
-        acc.z += v.z;
-        acc.w += v.w;
+    for (int i = 0; i < NT_O; ++i) {
+      o[i][0] *= f0;
+      o[i][1] *= f0;
+      o[i][2] *= f1;
+      o[i][3] *= f1;
+    }
+    // key-slice sum: warps ks >= 1 park their fragments in the CTA's global scratch (lane-major,
+    // coalesced), warps ks == 0 add them (L2 hits, L1 bypassed) and store their 16 rows
+    if (KS > 1) {
+      float* xs = p.ws_x + (size_t)blockIdx.x * XS_FRAGS * 16 * D;  // this CTA's fragment scratch
+      if (ks > 0) {
+        float* dst = xs + (size_t)(mt * (KS - 1) + ks - 1) * 16 * D;
+#pragma unroll
+        for (int i = 0; i < NT_O; ++i)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) __stcg(dst + (i * 4 + e) * 32 + lane, o[i][e]);
       }
-      const float lse2 = lsebuf[r];
-      if (complete) {
-        const int64_t orow = out_row(p, b, kvh, r);
-        *reinterpret_cast<float4*>(p.out + orow * D + c4) = acc;
-        if (c4 == 0 && p.lse != nullptr) p.lse[orow] = lse2 * LN2;
-      } else {
-        const int64_t prow = (int64_t)slot_base * p.R + r;
-        __stcg(reinterpret_cast<float4*>(p.ws_o + prow * D + c4), acc);
-        if (c4 == 0) __stcg(p.ws_lse + prow, lse2);
+      named_bar_sync(1, NC * 32);
+      if (ks == 0) {
+#pragma unroll
+        for (int k = 1; k < KS; ++k) {
+          const float* src = xs + (size_t)(mt * (KS - 1) + k - 1) * 16 * D;
+#pragma unroll
+          for (int i = 0; i < NT_O; ++i)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[i][e] += __ldcg(src + (i * 4 + e) * 32 + lane);
+        }
+      }
+    } else {
+      named_bar_sync(1, NC * 32);  // lsebuf
+    }
+    // rows r < R -> the final output, or this chunk's partial slot
+    const bool complete = sg.complete();
+    const int slot_base = chunk * 2 + pl.slot(sg.ustart, chunk);
+    if (ks == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = mt * 16 + gq + h * 8;
+        if (r < p.R) {
+          float* dst;
+          if (complete) {
+            const int64_t orow = out_row(p, b, kvh, r);
+            dst = p.out + orow * D;
+            if (cq == 0 && p.lse != nullptr) p.lse[orow] = lsebuf[r] * LN2;
+          } else {
+            const int64_t prow = (int64_t)slot_base * p.R + r;
+            dst = p.ws_o + prow * D;
+            if (cq == 0) __stcg(p.ws_lse + prow, lsebuf[r]);
+          }
+#pragma unroll
+          for (int i = 0; i < NT_O; ++i)
+            __stcg(reinterpret_cast<float2*>(dst + i * 8 + cq * 2), make_float2(o[i][2 * h], o[i][2 * h + 1]));
+        }
       }
     }
     if (!complete && p.fused_merge) finish_unit<D>(p, sg, pl, NC * 32, flag);
-    fence_proxy_async();         // order our generic writes to the ring before later TMA writes
-    named_bar_sync(1, NC * 32);  // the scratch (= ring) may now be refilled
-    if (lane == 0) mbar_arrive(epi_done);
+    named_bar_sync(1, NC * 32);  // mlbuf / lsebuf / scratch reused by the next segment
     trace_stamp(p, 5);
+  }
+  // the last CTA to finish re-arms the dynamic counters for the next call
+  if (pl.nch > pl.G && threadIdx.x == 0) {
+    if (atomicAdd(p.dyn + 1, 1) == pl.G - 1) {
+      p.dyn[0] = 0;
+      p.dyn[1] = 0;
+    }
   }
 }
 
@@ -828,7 +898,8 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   uint64_t* cempty = cfull + 2;
   int* cids = reinterpret_cast<int*>(cempty + 2);
   int* flag = cids + 2;  // [4] finish_unit
-  int* pre = flag + 4;  // [TABLE_B + 1] per-sequence tile prefix
+  Plan* plan_smem = reinterpret_cast<Plan*>(flag + 4);  // 40 bytes (reserved 48)
+  int* pre = flag + 16;  // [TABLE_B + 1] per-sequence tile prefix
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -855,7 +926,10 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   trace_stamp(p, 1);
   __syncthreads();
   build_prefix(p, pre);
-  const Plan pl = make_plan(p, total_tiles(p, pre), gridDim.x);
+  // the plan lives in shared memory (read only at segment boundaries: keeps registers free)
+  if (threadIdx.x == 0) *plan_smem = make_plan(p, total_tiles(p, pre), gridDim.x);
+  __syncthreads();
+  const Plan& pl = *plan_smem;
   if ((int)blockIdx.x >= pl.G) return;  // uniform across the CTA
   int chunk = blockIdx.x;                // this CTA's static chunk, then claimed dynamic ones
   SegWalker walk;
@@ -883,7 +957,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     int ahead = 0;
     if (pl.nch > pl.G && lane == 0) ahead = atomicAdd(p.dyn, 1);
     auto next_seg = [&]() -> bool {
-      while (!walk.next(p, sg)) {
+      while (!walk.next(p, pre, sg)) {
         if (pl.nch == pl.G) return false;
         int nxt = -1;
         if (lane == 0) {
@@ -927,7 +1001,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   int it = 0, qi = 0, ck = 0;
   unsigned long long qi_seg = 0;
   auto next_seg = [&]() -> bool {  // mirrors the producer's chunk sequence
-    while (!walk.next(p, sg)) {
+    while (!walk.next(p, pre, sg)) {
       if (pl.nch == pl.G) return false;
       const int cs = ck & 1;
       mbar_wait(&cfull[cs], (ck >> 1) & 1);
@@ -1219,8 +1293,11 @@ static int grid_for(int R, int sm_count) {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// Dynamic chunks per active CTA (keys kernel only; the rows kernel's epilogue aliases its
-// ring, so extra segment boundaries would stall its producer): MD_DYN_K, default 4.
+// Dynamic chunks per active CTA (MD_DYN_K, default 4; only used by long calls, see make_plan).
+// Keys kernel only: its consumers are lightly loaded and get Q from the producer, so the
+// extra segment boundaries are cheap; the rows kernel (HMMA-heavy consumers that fetch Q at
+// each segment) measured slower with dynamic chunks (Llama verify 1.23 -> 1.34 ms) and its
+// static stream-K spread is small once the epilogue no longer stalls the producer.
 static int dyn_k_for(int R) {
   static const int k = env_int("MD_DYN_K", 4);
   return use_keys_kernel(R) ? (k < 0 ? 0 : k) : 0;
@@ -1243,7 +1320,8 @@ constexpr size_t COUNTER_BYTES = ((size_t)(MAX_UNITS + 2) * 4 + 255) & ~size_t(2
 static size_t workspace_for(int G, int units, int R, int D) {
   (void)units;
   const size_t C = (size_t)G * (1 + dyn_k_for(R));
-  return COUNTER_BYTES + align256(C * 2 * R * D * 4) + align256(C * 2 * R * 4);
+  const size_t X = use_keys_kernel(R) ? 0 : (size_t)G * XS_FRAGS * 16 * D * 4;  // rows-kernel scratch
+  return COUNTER_BYTES + align256(C * 2 * R * D * 4) + align256(C * 2 * R * 4) + align256(X);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -1433,6 +1511,8 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.ws_o = reinterpret_cast<float*>(w);
   w += align256(chunks * 2 * R * c->head_dim * 4);
   p.ws_lse = reinterpret_cast<float*>(w);
+  w += align256(chunks * 2 * R * 4);
+  p.ws_x = use_keys_kernel(R) ? nullptr : reinterpret_cast<float*>(w);
   st = (c->head_dim == 128) ? launch_dim<128>(tm, p, grid, s) : launch_dim<64>(tm, p, grid, s);
   if (st != MD_OK || p.fused_merge) return st;
   if (c->head_dim == 128)
