@@ -1300,7 +1300,8 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // static stream-K spread is small once the epilogue no longer stalls the producer.
 static int dyn_k_for(int R) {
   static const int k = env_int("MD_DYN_K", 4);
-  return use_keys_kernel(R) ? (k < 0 ? 0 : k) : 0;
+  static const int rows = env_int("MD_DYN_ROWS", 0);  // 1: also the rows kernel (tests, experiments)
+  return (use_keys_kernel(R) || rows) ? (k < 0 ? 0 : k) : 0;
 }
 static int dyn_min_tiles() {  // 128 tiles = 8 MB of K+V per CTA at d = 128 (MD_DYN_MIN)
   static const int v = env_int("MD_DYN_MIN", 128);
