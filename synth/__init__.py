@@ -242,3 +242,33 @@ def sigma_for_overlap(seed: int, V: int, target: float, rows: int = 4, zipf_s: f
         else:
             hi = mid
     return 0.5 * (lo + hi)
+
+
+# ----------------------------------------------------------------------------------------
+# PQCache codebooks.  The codebook is trained at prefill (k-means,
+# outside the decode hot path); the synthetic stand-in takes centroid c of sub-space m to be
+# sub-vector m of the unit's own key at a hashed prompt position (the usual k-means
+# initialisation), so it lies on the same exact bf16 grid as the keys.
+# ----------------------------------------------------------------------------------------
+T_PQCB = 13
+PQ_M, PQ_C = 16, 256
+
+
+def pq_codebook_positions(seed: int, B: int, Hkv: int, L) -> np.ndarray:
+    """int64 [B, Hkv, 16, 256]: prompt position (in [0, L_b)) whose key sub-vector m seeds
+    centroid c."""
+    L = np.asarray(L, dtype=np.int64).reshape(B)
+    b, u, m, c = np.meshgrid(np.arange(B), np.arange(Hkv), np.arange(PQ_M), np.arange(PQ_C), indexing="ij")
+    idx = (((b * Hkv + u) * PQ_M + m) * PQ_C + c).astype(U64)
+    return (hash_u64(seed, T_PQCB, idx) % L[b].astype(U64)).astype(np.int64)
+
+
+def pq_codebook_bits(k_bits: np.ndarray, positions: np.ndarray) -> np.ndarray:
+    """bf16 bits [B, Hkv, 16, 256, d/16]: gathered key sub-vectors (k_bits [B, Hkv, cap, d])."""
+    B, Hkv, _, d = k_bits.shape
+    s = d // PQ_M
+    b, u, c = np.meshgrid(np.arange(B), np.arange(Hkv), np.arange(PQ_C), indexing="ij")
+    out = np.empty((B, Hkv, PQ_M, PQ_C, s), dtype=np.uint16)
+    for mm in range(PQ_M):
+        out[:, :, mm] = k_bits[b, u, positions[:, :, mm], mm * s:(mm + 1) * s]
+    return out
