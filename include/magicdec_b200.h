@@ -15,6 +15,7 @@
  *   md_draft_attn_sparse  1 query token / sequence over sink ∪ window (no KV copy)
  *   md_draft_attn_indexed 1 query token / sequence over a SnapKV index list ∪ recent tail
  *   md_snapkv_select      prefill-time SnapKV selection of that index list
+ *   md_pq_encode / md_pq_select  PQCache-style dynamic selection of that list per query
  *   md_verify_attn_full   gamma+1 query tokens / sequence over the full KV, GQA, causal
  *   md_spec_accept        batched acceptance + residual / bonus resampling (or greedy)
  *   md_philox_u32         counter-based uniforms feeding md_spec_accept
@@ -228,6 +229,59 @@ MD_API md_status md_snapkv_select(const md_kv_cache* cache, const void* q_obs, i
                                   const int32_t* prefill_len, int32_t max_prefill_len, int32_t w, int32_t budget,
                                   float scale, int32_t* idx, int32_t idx_stride, int32_t* idx_count, void* workspace,
                                   size_t workspace_bytes, md_stream_t stream);
+
+/*
+ * PQCache-style dynamic KV selection.  Dynamic methods "search the KV
+ * cache for each input query, attempting to find the top k nearest neighbors";
+ * PQCache "employs product quantization with 16 sub-vectors and 8-bit quantization per key
+ * vector" (P:1141 footnote); its search is the T_select term of Eq.3.  Keys are
+ * cut into 16 sub-vectors of s = head_dim/16 elements, each coded by the index of its
+ * nearest of 256 centroids; a draft query scores every candidate key through a lookup table
+ * of query-centroid inner products, and the top-scoring positions plus the sink rows form
+ * the index list of md_draft_attn_indexed (with the recent window as its streamed tail).
+ * Readings Z25-Z29; oracle/pqcache.py P1-P5.
+ *
+ * codebook: device bf16 [B][Hkv][16][256][s] (trained at prefill by the caller, e.g.
+ *           k-means; not part of the decode path), 16-byte aligned.
+ * codes:    device uint8 [B][Hkv][code_capacity][16], 16-byte aligned.
+ *
+ * md_pq_encode — codes[b][h][start_pos[b] + t][m] for t < count, every KV head h and
+ * sub-space m: the index c of the centroid minimising sum_{i<s} (x_i - C[m][c][i])^2, the sum
+ * evaluated left to right with every operation rounded to fp32 (no fused multiply-add); ties
+ * -> lowest c.  Called once at prefill (count = prompt length) and then for rows about to
+ * leave the recent window (rows inside it are attended exactly, so encoding can be lazy).
+ * Preconditions (device): start_pos[b] + count <= min(capacity, code_capacity).
+ */
+MD_API md_status md_pq_encode(const md_kv_cache* cache, const void* codebook, const int32_t* start_pos,
+                              int32_t count, uint8_t* codes, int32_t code_capacity, md_stream_t stream);
+
+/*
+ * md_pq_select — per draft query, for every sequence b (n = kv_len[b]) and KV head u:
+ *   lut[m][c]  = sum_{hh<g} sum_{i<s} q[b][u*g+hh][m*s+i] * C[m][c][i]   (fp32, hh outer, i
+ *                inner, left to right, no FMA; the GQA group shares one selection);
+ *   lutq       = rint(lut * 2^e) as int32, e = 26 - E with max|lut| = f*2^E, f in [0.5, 1)
+ *                (e = 0 for an all-zero table) — exact power-of-two scaling;
+ *   score[j]   = sum_m lutq[m][code[j][m]]   (exact integer);
+ *   s0 = min(sink, n), tail = max(s0, n - window), c = min(budget, tail - s0);
+ *   idx[b][u][0 .. s0 + c) = 0 .. s0-1, then the c positions of [s0, tail) with the largest
+ *   score (ties -> lower position) in ascending order; idx_count[b] = s0 + c;
+ *   tail_start[b] = tail.  Entries past s0 + c are left untouched.
+ * Then md_draft_attn_indexed(idx, idx_stride, idx_count, tail_start) attends to
+ * idx U [tail, n).  Every decision is taken on exact integers, so the lists are bit-exact.
+ *   q: device bf16 [B][Hq][head_dim] (the draft query); kv_len: device int32[B];
+ *   max_kv_len: host bound >= every kv_len[b], <= code_capacity;
+ *   idx: device int32 [B][Hkv][idx_stride], idx_stride >= sink + budget (a multiple of 4
+ *        for md_draft_attn_indexed); idx_count, tail_start: device int32[B];
+ *   workspace: >= md_pq_workspace_bytes(B, Hkv, max_kv_len) bytes (no initialisation).
+ * Supported: head_dim in {64, 128}, g <= 16.
+ * Preconditions (device): kv_len[b] <= max_kv_len; codes of [0, tail) encoded.
+ */
+MD_API size_t md_pq_workspace_bytes(int32_t batch, int32_t num_kv_heads, int32_t max_kv_len);
+MD_API md_status md_pq_select(const void* q, int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
+                              int32_t head_dim, const void* codebook, const uint8_t* codes, int32_t code_capacity,
+                              const int32_t* kv_len, int32_t max_kv_len, int32_t sink, int32_t window,
+                              int32_t budget, int32_t* idx, int32_t idx_stride, int32_t* idx_count,
+                              int32_t* tail_start, void* workspace, size_t workspace_bytes, md_stream_t stream);
 
 /*
  * md_philox_u32 — Philox4x32-10 uniforms for md_spec_accept (

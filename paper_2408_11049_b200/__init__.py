@@ -8,7 +8,8 @@ tensor raises.
 Functions mirror the C calls (same names without the `md_` prefix):
     kv_append, attn_workspace_bytes, verify_attn_full, draft_attn_sparse,
     draft_attn_indexed, snapkv_workspace_bytes, snapkv_select, philox_u32, spec_accept,
-    verify_attn_tree, spec_accept_tree, kv_compact (tree speculation)
+    verify_attn_tree, spec_accept_tree, kv_compact (tree speculation),
+    pq_encode, pq_workspace_bytes, pq_select (PQCache dynamic selection)
 """
 from __future__ import annotations
 
@@ -27,7 +28,8 @@ MD_ACCEPT_SAMPLE, MD_ACCEPT_GREEDY = 0, 1
 ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_workspace_bytes",
                "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed", "md_snapkv_workspace_bytes",
                "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace",
-               "md_verify_attn_tree", "md_spec_accept_tree", "md_kv_compact")
+               "md_verify_attn_tree", "md_spec_accept_tree", "md_kv_compact", "md_pq_encode", "md_pq_workspace_bytes",
+               "md_pq_select")
 
 
 class MDError(RuntimeError):
@@ -83,9 +85,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.md_spec_accept_tree.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, i32, i32, i32,
                                         ctypes.c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
     lib.md_kv_compact.argtypes = [pc, c_void_p, c_void_p, i32, c_void_p, c_void_p]
+    lib.md_pq_encode.argtypes = [pc, c_void_p, c_void_p, i32, c_void_p, i32, c_void_p]
+    lib.md_pq_workspace_bytes.argtypes = [i32, i32, i32]
+    lib.md_pq_workspace_bytes.restype = sz
+    lib.md_pq_select.argtypes = [c_void_p, i32, i32, i32, i32, c_void_p, c_void_p, i32, c_void_p, i32, i32, i32, i32,
+                                 c_void_p, i32, c_void_p, c_void_p, c_void_p, sz, c_void_p]
     for name in ("md_kv_append", "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed",
                  "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace", "md_verify_attn_tree",
-                 "md_spec_accept_tree", "md_kv_compact"):
+                 "md_spec_accept_tree", "md_kv_compact", "md_pq_encode", "md_pq_select"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -200,6 +207,34 @@ def snapkv_select(k_cache, v_cache, q_obs, prefill_len, max_prefill_len, w, budg
     _check(lib.md_snapkv_select(ctypes.byref(c), _ptr(q_obs), q_obs.shape[2], _ptr(prefill_len), int(max_prefill_len),
                                 int(w), int(budget), float(scale), _ptr(idx), idx.shape[2], _ptr(idx_count), ws, wsb,
                                 _stream(stream)))
+
+
+def pq_encode(k_cache, v_cache, codebook, start_pos, count, codes, stream=None):
+    """PQ codes of cache rows [start_pos[b], start_pos[b] + count): codebook [B, Hkv, 16, 256, d/16] bf16,
+    codes [B, Hkv, code_cap, 16] uint8."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    _check(lib.md_pq_encode(ctypes.byref(c), _ptr(codebook), _ptr(start_pos), int(count), _ptr(codes),
+                            codes.shape[2], _stream(stream)))
+
+
+def pq_workspace_bytes(batch, num_kv_heads, max_kv_len) -> int:
+    return int(load_library().md_pq_workspace_bytes(batch, num_kv_heads, max_kv_len))
+
+
+def pq_select(q, codebook, codes, kv_len, max_kv_len, sink, window, budget, idx, idx_count, tail_start,
+              workspace=None, stream=None):
+    """Dynamic PQ selection for the draft query q [B, Hq, d] bf16 -> idx [B, Hkv, K] int32 (sink rows then
+    the top-`budget` candidates ascending; K >= sink + budget), idx_count [B], tail_start [B]."""
+    lib = load_library()
+    B, Hq, d = q.shape
+    Hkv = codebook.shape[1]
+    if workspace is None:
+        workspace = torch.empty(pq_workspace_bytes(B, Hkv, max_kv_len), dtype=torch.uint8, device=q.device)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_pq_select(_ptr(q), B, Hq, Hkv, d, _ptr(codebook), _ptr(codes), codes.shape[2], _ptr(kv_len),
+                            int(max_kv_len), int(sink), int(window), int(budget), _ptr(idx), idx.shape[2],
+                            _ptr(idx_count), _ptr(tail_start), ws, wsb, _stream(stream)))
 
 
 def philox_u32(seed, step, out, stream=None):
