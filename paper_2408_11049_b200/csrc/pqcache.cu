@@ -14,10 +14,11 @@
 //                     of a warp always hit 32 different banks (lane l reads sub-space
 //                     (i ^ l) & 15 at step i, from copy l >> 4 of the table, and table m
 //                     lives in bank m (copy 0) / 16 + m (copy 1));
-//   pq_select_kernel  top-c of [s0, tail) by score (ties -> lower position): 4-pass 8-bit
-//                     radix select on order-preserving uint32 keys, then an ordered
-//                     compaction over per-thread contiguous runs (two block scans); the
-//                     candidate scores are staged in shared memory when they fit.
+//   pq_select_kernel  top-c of [s0, tail) by score (ties -> lower position): radix select
+//                     on order-preserving uint32 keys (12 + 10 + 10-bit digits; after the
+//                     first pass only the keys of the cutoff bin are kept, in shared
+//                     memory), then an ordered compaction over per-thread contiguous runs
+//                     (two block scans).  The scores are read from L2.
 // Integer scores make every selection decision exact and independent of summation order, so
 // the index lists equal the oracle's bit for bit (oracle/pqcache.py P1-P5).
 #include <cuda.h>
@@ -32,12 +33,34 @@ namespace pq {
 
 constexpr int M = 16;      // sub-vectors per key
 constexpr int NC = 256;    // centroids per sub-space (8-bit codes)
-constexpr int SCORE_CH = 4096;   // keys per score CTA
-constexpr int SCORE_THREADS = 256;
-constexpr int SEL_THREADS = 1024;
-constexpr int SEL_SMEM_MAX = 49152;  // candidate scores staged in smem up to this count
+constexpr int SCORE_CH = 16384;  // candidates per score CTA
+constexpr int SCORE_THREADS = 512;
+constexpr int NS = 5;            // cp.async pipeline depth of the score kernel (keys per thread)
+constexpr int SCORE_SMEM = NC * 64 * 4 + 1024 * 4 + NS * SCORE_THREADS * 16;  // table + histogram + ring
+constexpr int HIST1 = 1024;      // pass-1 digit: key bits 31..22
+constexpr int HIST2 = 2048;      // passes 2, 3: bits 21..11, 10..0
+constexpr int TIE_CAP = 2048;    // keys of the cutoff bin kept in shared memory
+constexpr int SEL_THREADS = 512;
+constexpr int RL = 36;           // candidates per select thread run (16-byte loads, no bank conflicts)
+constexpr int SB = SEL_THREADS * RL;  // candidates staged in shared memory per super-block
+constexpr int SEL_SMEM = SB * 4 + TIE_CAP * 6;
 
 __device__ __forceinline__ float bf16_to_f32(uint16_t b) { return __uint_as_float(static_cast<uint32_t>(b) << 16); }
+
+// per-thread 16-byte async copies global -> shared (each thread later reads only its own slots)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
 
 // ------------------------------------------------------------------ P1 encode
 // grid (units, 16 sub-spaces), 256 threads; centroids of (unit, m) in smem as fp32.
@@ -101,7 +124,8 @@ __global__ void __launch_bounds__(256) pq_encode_kernel(const uint16_t* __restri
 // grid units, 256 threads: thread c computes lut[m][c] for all 16 m.
 template <int S>
 __global__ void __launch_bounds__(256) pq_lut_kernel(const uint16_t* __restrict__ q, int Hq, int Hkv,
-                                                     const uint16_t* __restrict__ cb, int32_t* __restrict__ lutq) {
+                                                     const uint16_t* __restrict__ cb, int32_t* __restrict__ lutq,
+                                                     uint32_t* __restrict__ hist) {
   constexpr int D = S * M;
   extern __shared__ float qs[];  // [g][D]
   __shared__ float red[8];
@@ -116,12 +140,27 @@ __global__ void __launch_bounds__(256) pq_lut_kernel(const uint16_t* __restrict_
   const uint16_t* cbu = cb + (size_t)unit * M * NC * S;
   float lut[M];
   float mx = 0.f;
+  // all 16 centroid rows of this thread up front (16-byte loads, independent)
+  uint32_t cw[M][S / 2];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const uint16_t* src = cbu + ((size_t)m * NC + c) * S;
+    if constexpr (S == 8) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(src));
+      cw[m][0] = w.x; cw[m][1] = w.y; cw[m][2] = w.z; cw[m][3] = w.w;
+    } else {
+      const uint2 w = __ldg(reinterpret_cast<const uint2*>(src));
+      cw[m][0] = w.x; cw[m][1] = w.y;
+    }
+  }
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     float cen[S];
-    const uint16_t* src = cbu + ((size_t)m * NC + c) * S;
 #pragma unroll
-    for (int i = 0; i < S; ++i) cen[i] = bf16_to_f32(src[i]);
+    for (int i = 0; i < S / 2; ++i) {
+      cen[2 * i] = __uint_as_float(cw[m][i] << 16);
+      cen[2 * i + 1] = __uint_as_float(cw[m][i] & 0xffff0000u);
+    }
     float acc = 0.f;
     for (int hh = 0; hh < g; ++hh) {
 #pragma unroll
@@ -145,75 +184,112 @@ __global__ void __launch_bounds__(256) pq_lut_kernel(const uint16_t* __restrict_
   }
   int32_t* dst = lutq + (size_t)unit * M * NC;
 #pragma unroll
-  for (int m = 0; m < M; ++m) dst[m * NC + c] = __float2int_rn(ldexpf(lut[m], e));
+  for (int m = 0; m < M; ++m) dst[c * M + m] = __float2int_rn(ldexpf(lut[m], e));  // [c][m]
+  // the unit's pass-1 histogram, accumulated by the score kernel
+  for (int i = threadIdx.x; i < HIST1; i += blockDim.x) hist[(size_t)unit * HIST1 + i] = 0u;
 }
 
 // ------------------------------------------------------------------ P4 scores
-// grid (units, chunks of SCORE_CH keys); scores of the candidates [s0, tail) only.
-__global__ void __launch_bounds__(SCORE_THREADS) pq_score_kernel(const uint8_t* __restrict__ codes, int code_cap,
+__device__ __forceinline__ uint32_t okey(int32_t v) { return static_cast<uint32_t>(v) ^ 0x80000000u; }
+
+// grid (units, chunks of SCORE_CH candidates), SCORE_THREADS threads, dynamic smem = the
+// table (64 KB) + the pass-1 histogram.  Scores of the candidates [s0, tail) are stored
+// densely (candidate j - s0) and the top digit (bits 31..22 of the order-preserving key) of
+// every score is counted into the unit's global histogram.
+__global__ void __launch_bounds__(SCORE_THREADS, 2) pq_score_kernel(const uint8_t* __restrict__ codes, int code_cap,
                                                                  const int32_t* __restrict__ lutq,
                                                                  const int32_t* __restrict__ kv_len, int Hkv, int sink,
                                                                  int window, int32_t* __restrict__ scores,
-                                                                 int score_stride) {
-  // tab[c * 32 + copy * 16 + m] = lutq[m][c]: table m in bank m (copy 0) / 16 + m (copy 1)
-  __shared__ int32_t tab[NC * 32];
+                                                                 int score_stride, uint32_t* __restrict__ hist_g) {
+  // tab[c * 64 + copy * 16 + m] = lutq[m][c] (256-byte rows): table m lives in bank m (copy 0)
+  // and 16 + m (copy 1), and the byte offset of code c is c << 8 (one byte permute)
+  extern __shared__ int32_t tab[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(tab + NC * 64);
   pdl_trigger();
   pdl_wait();
   const int unit = blockIdx.x;
   const int b = unit / Hkv;
   const int n = __ldg(kv_len + b);
   const int s0 = min(sink, n), tail = max(s0, n - window);
-  const int lo = max(s0, (int)blockIdx.y * SCORE_CH), hi = min(tail, (int)(blockIdx.y + 1) * SCORE_CH);
+  const int lo = s0 + (int)blockIdx.y * SCORE_CH, hi = min(tail, lo + SCORE_CH);
   if (lo >= hi) return;  // uniform
   const int32_t* src = lutq + (size_t)unit * M * NC;
-  for (int i = threadIdx.x; i < M * NC; i += blockDim.x) {
-    const int m = i / NC, c = i - m * NC;
+  for (int i = threadIdx.x; i < M * NC; i += SCORE_THREADS) {  // lutq is [c][m]: coalesced, <= 2-way stores
+    const int c = i >> 4, m = i & 15;
     const int32_t v = __ldg(src + i);
-    tab[c * 32 + m] = v;
-    tab[c * 32 + 16 + m] = v;
+    tab[c * 64 + m] = v;
+    tab[c * 64 + 16 + m] = v;
   }
+  for (int i = threadIdx.x; i < HIST1; i += SCORE_THREADS) hist[i] = 0u;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int l15 = lane & 15;
   const uint32_t tbase = smem_u32(tab) + ((lane >> 4) << 6);  // copy (lane >> 4): +16 words
-  // per-lane constant part of the address of step i: ((i ^ l15) << 2), sub-space m = i ^ l15
+  // step i reads sub-space m = i ^ l15: its byte is byte ((i & 3) ^ rx) of word ((i >> 2) ^ qx)
   uint32_t off[M];
 #pragma unroll
   for (int i = 0; i < M; ++i) off[i] = tbase + (uint32_t)((i ^ l15) << 2);
-  // the byte of sub-space (i ^ l15) sits in word ((i >> 2) ^ q) at byte ((i & 3) ^ r)
   const int qx = l15 >> 2, rx = l15 & 3;
+  uint32_t sel[4];  // byte permute selectors: byte ((k ^ rx)) of the word -> bits 15..8, zeros elsewhere
+#pragma unroll
+  for (int k = 0; k < 4; ++k) sel[k] = 0x4404u | ((uint32_t)(k ^ rx) << 4);
   const uint4* crow = reinterpret_cast<const uint4*>(codes + (size_t)unit * code_cap * M);
-  int32_t* out = scores + (size_t)unit * score_stride;
-  for (int j = lo + threadIdx.x; j < hi; j += SCORE_THREADS) {
-    const uint4 w4 = __ldcs(crow + j);  // streamed once
-    uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-    // word permutation w'[i] = w[i ^ qx] (two conditional swap stages)
-    if (qx & 1) {
-      uint32_t t = w[0]; w[0] = w[1]; w[1] = t;
-      t = w[2]; w[2] = w[3]; w[3] = t;
-    }
-    if (qx & 2) {
-      uint32_t t = w[0]; w[0] = w[2]; w[2] = t;
-      t = w[1]; w[1] = w[3]; w[3] = t;
-    }
+  int32_t* out = scores + (size_t)unit * score_stride - s0;
+  // the 4 code words of a slot read in the order w'[i] = w[i ^ qx] (per-lane byte offsets)
+  uint32_t woff[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) woff[i] = (uint32_t)((i ^ qx) << 2);
+  auto score_one = [&](uint32_t slot) -> int32_t {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w[i]) : "r"(slot + woff[i]));
     int32_t acc = 0;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-      const uint32_t code = (w[i >> 2] >> (((i & 3) ^ rx) << 3)) & 0xffu;
       int32_t v;
-      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(off[i] + (code << 7)));
+      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(off[i] + __byte_perm(w[i >> 2], 0u, sel[i & 3])));
       acc += v;
     }
-    out[j] = acc;
+    return acc;
+  };
+  auto emit = [&](int j, int32_t sc) {
+    out[j] = sc;
+    atomicAdd(&hist[okey(sc) >> 22], 1u);
+  };
+  // per-thread NS-deep cp.async pipeline: the codes of this thread's next NS - 1 keys are in
+  // flight while it scores the current one (each thread reads only the slots it filled)
+  const uint32_t ring = smem_u32(hist + HIST1) + threadIdx.x * 16;
+  const int j0 = lo + threadIdx.x;
+  const int nk = j0 < hi ? (hi - j0 + SCORE_THREADS - 1) / SCORE_THREADS : 0;
+#pragma unroll
+  for (int k = 0; k < NS - 1; ++k) {
+    if (k < nk) cp_async16(ring + k * SCORE_THREADS * 16, crow + j0 + k * SCORE_THREADS);
+    cp_async_commit();
+  }
+  int rd = 0, wr = NS - 1;
+  for (int i = 0; i < nk; ++i) {
+    if (i + NS - 1 < nk) cp_async16(ring + wr * SCORE_THREADS * 16, crow + j0 + (i + NS - 1) * SCORE_THREADS);
+    cp_async_commit();
+    cp_async_wait<NS - 1>();
+    emit(j0 + i * SCORE_THREADS, score_one(ring + rd * SCORE_THREADS * 16));
+    rd = rd == NS - 1 ? 0 : rd + 1;
+    wr = wr == NS - 1 ? 0 : wr + 1;
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  uint32_t* hg = hist_g + (size_t)unit * HIST1;
+  for (int i = threadIdx.x; i < HIST1; i += SCORE_THREADS) {
+    const uint32_t v = hist[i];
+    if (v) atomicAdd(hg + i, v);
   }
 }
 
 // ------------------------------------------------------------------ P5 selection
-__device__ __forceinline__ uint32_t okey(int32_t s) { return static_cast<uint32_t>(s) ^ 0x80000000u; }
-
-// exclusive block scan of one value per thread (SEL_THREADS threads)
-__device__ __forceinline__ uint32_t sel_excl_scan(uint32_t v, uint32_t* sm, uint32_t& total) {
+// exclusive block scan of one value per thread (NT threads, NT / 32 <= 32 warps)
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sm, uint32_t& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = NT / 32;
   uint32_t incl = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -224,7 +300,7 @@ __device__ __forceinline__ uint32_t sel_excl_scan(uint32_t v, uint32_t* sm, uint
   if (lane == 31) sm[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    uint32_t x = sm[lane];  // SEL_THREADS / 32 == 32 warps
+    const uint32_t x = lane < NW ? sm[lane] : 0u;
     uint32_t xi = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -241,19 +317,56 @@ __device__ __forceinline__ uint32_t sel_excl_scan(uint32_t v, uint32_t* sm, uint
   return r;
 }
 
-// padded smem index: run-contiguous reads by thread t (positions t*R + k) are conflict-free
-__device__ __forceinline__ int pad_idx(int i) { return i + (i >> 5); }
+// Find the bin holding the need-th largest key of a histogram (bins ascending by value):
+// the bin and how many keys of that bin are still needed.  Thread t owns nb / NT
+// consecutive bins counted from the top.
+template <int NT>
+__device__ __forceinline__ void find_cut(const uint32_t* hist, int nb, uint32_t need, uint32_t* sm, int* s_bin,
+                                         uint32_t* s_need) {
+  const int per = nb / NT;
+  const int top = nb - 1 - threadIdx.x * per;  // this thread's highest bin
+  uint32_t local = 0;
+  for (int i = 0; i < per; ++i) local += hist[top - i];
+  uint32_t total;
+  const uint32_t above = block_excl_scan<NT>(local, sm, total);
+  if (above < need && above + local >= need) {
+    uint32_t acc = above;
+    int bin = top;
+    for (int i = 0; i < per - 1; ++i, --bin) {
+      if (acc + hist[bin] >= need) break;
+      acc += hist[bin];
+    }
+    *s_bin = bin;
+    *s_need = need - acc;
+  }
+  __syncthreads();
+}
 
-template <bool SMEM>
-__global__ void __launch_bounds__(SEL_THREADS) pq_select_kernel(const int32_t* __restrict__ scores, int score_stride,
-                                                                const int32_t* __restrict__ kv_len, int Hkv, int sink,
-                                                                int window, int budget, int32_t* __restrict__ idx,
-                                                                int idx_stride, int32_t* __restrict__ idx_count,
-                                                                int32_t* __restrict__ tail_start) {
-  extern __shared__ uint32_t sel_sm[];  // staged keys (SMEM) — padded
-  __shared__ uint32_t hist[256];
+// One CTA per unit.  The pass-1 histogram (10-bit top digit) comes from the score kernel.
+// The candidate scores are staged in shared memory by one bulk copy per super-block of SB
+// candidates; thread t owns the contiguous run [t*RL, (t+1)*RL) of it (RL = 36: the 16-byte
+// loads of 8 consecutive threads hit disjoint banks).  Pass over the runs: count the keys above
+// the cutoff bin and gather the cutoff bin's keys (with their owner thread) into a small list;
+// passes 2-3 (11 + 11 bits) refine the threshold key thr and how many keys equal to thr to
+// take (the lowest positions) on that list, which also yields every thread's count of
+// selected keys; an exclusive scan of the counts then places each run's selections in
+// position order (second pass over the runs).  A cutoff bin with more than TIE_CAP keys is
+// refined from global memory instead.
+__global__ void __launch_bounds__(SEL_THREADS, 2) pq_select_kernel(const int32_t* __restrict__ scores,
+                                                                   int score_stride, const uint32_t* __restrict__ hist_g,
+                                                                   const int32_t* __restrict__ kv_len, int Hkv, int sink,
+                                                                   int window, int budget, int32_t* __restrict__ idx,
+                                                                   int idx_stride, int32_t* __restrict__ idx_count,
+                                                                   int32_t* __restrict__ tail_start) {
+  extern __shared__ __align__(16) int32_t stage[];  // [SB] staged scores, ties[TIE_CAP], owner[TIE_CAP]
+  uint32_t* ties = reinterpret_cast<uint32_t*>(stage + SB);
+  uint16_t* owner = reinterpret_cast<uint16_t*>(ties + TIE_CAP);
+  __shared__ uint32_t hist[HIST2];
+  __shared__ uint32_t n_gt_sm[SEL_THREADS], n_eq_sm[SEL_THREADS];
   __shared__ uint32_t scan_sm[65];
-  __shared__ uint32_t s_prefix, s_need;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int s_bin;
+  __shared__ uint32_t s_need, s_nties;
   pdl_trigger();
   pdl_wait();
   const int unit = blockIdx.x;
@@ -274,97 +387,146 @@ __global__ void __launch_bounds__(SEL_THREADS) pq_select_kernel(const int32_t* _
     for (int j = threadIdx.x; j < cnt; j += SEL_THREADS) out[j] = s0 + j;
     return;
   }
-  const int32_t* sc = scores + (size_t)unit * score_stride + s0;
-  if constexpr (SMEM) {
-    for (int j = threadIdx.x; j < cnt; j += SEL_THREADS) sel_sm[pad_idx(j)] = okey(__ldcg(sc + j));
+  const int32_t* sc = scores + (size_t)unit * score_stride;  // candidate j at sc[j] (16-byte aligned)
+  // ---- pass 1 (histogram from the score kernel): cutoff bin of the top digit
+  {
+    const uint32_t* hg = hist_g + (size_t)unit * HIST1;
+    for (int i = threadIdx.x; i < HIST1; i += SEL_THREADS) hist[i] = __ldcg(hg + i);
+    if (threadIdx.x == 0) {
+      s_nties = 0;
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+    }
     __syncthreads();
   }
-  auto key_at = [&](int j) -> uint32_t {
-    if constexpr (SMEM) return sel_sm[pad_idx(j)];
-    else return okey(__ldcg(sc + j));
+  find_cut<SEL_THREADS>(hist, HIST1, (uint32_t)c, scan_sm, &s_bin, &s_need);
+  const uint32_t cb = (uint32_t)s_bin;
+  uint32_t prefix = cb << 22, need = s_need;
+  const uint32_t nbin = hist[cb];
+  const bool gathered = nbin <= TIE_CAP;
+  const int nsb = (cnt + SB - 1) / SB;
+  uint32_t phase = 0;
+  auto stage_block = [&](int base) {  // candidates [base, base + SB) -> stage (one bulk copy)
+    const int nb = min(SB, cnt - base);
+    __syncthreads();  // every reader of the previous super-block is done
+    if (threadIdx.x == 0) {
+      fence_proxy_async();  // earlier generic reads of the stage before the async-proxy overwrite
+      const uint32_t bytes = (uint32_t)((nb + 3) & ~3) * 4;  // rows are padded to 4 candidates
+      mbar_arrive_expect_tx(&bar, bytes);
+      bulk_load(stage, sc + base, bytes, &bar);
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    return nb;
   };
-  // radix select of the c-th largest key
-  if (threadIdx.x == 0) {
-    s_prefix = 0;
-    s_need = c;
-  }
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += SEL_THREADS) hist[i] = 0;
-    __syncthreads();
-    const uint32_t pre = s_prefix;
-    const uint32_t mask = (shift == 24) ? 0u : (0xffffffffu << (shift + 8));
-    for (int j = threadIdx.x; j < cnt; j += SEL_THREADS) {
-      const uint32_t kk = key_at(j);
-      if ((kk & mask) == (pre & mask)) {
-        const uint32_t bin = (kk >> shift) & 255u;
-        // aggregate equal bins within the warp: one shared atomic per distinct bin
-        const unsigned act = __activemask();
-        const unsigned peers = __match_any_sync(act, bin);
-        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+  // run loop: f(k, key) for this thread's valid candidates of the staged super-block
+  auto for_run = [&](int nb, auto&& f) {
+    const int r0 = threadIdx.x * RL;
+    if (r0 + RL <= nb) {
+#pragma unroll 3
+      for (int k = 0; k < RL; k += 4) {
+        const int4 x = *reinterpret_cast<const int4*>(stage + r0 + k);
+        f(r0 + k, okey(x.x));
+        f(r0 + k + 1, okey(x.y));
+        f(r0 + k + 2, okey(x.z));
+        f(r0 + k + 3, okey(x.w));
       }
+    } else {
+      for (int k = r0; k < nb; ++k) f(k, okey(stage[k]));
     }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      // warp 0 finds the bin holding the need-th largest: suffix sums over 8 bins per lane
-      const int lane = threadIdx.x;
-      uint32_t cnt8 = 0;
-#pragma unroll
-      for (int t = 0; t < 8; ++t) cnt8 += hist[lane * 8 + t];
-      // inclusive suffix sum over lanes (lane 31 holds the top bins)
-      uint32_t suf = cnt8;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_down_sync(0xffffffffu, suf, o);
-        if (lane + o < 32) suf += t;
-      }
-      const uint32_t need = s_need;
-      const uint32_t above = suf - cnt8;  // keys in higher lanes' bins
-      if (above < need && suf >= need) {  // exactly one lane
-        uint32_t acc = above;
-        int bin = lane * 8 + 7;
-        for (; bin > lane * 8; --bin) {
-          if (acc + hist[bin] >= need) break;
-          acc += hist[bin];
+  };
+  // ---- runs pass 1: keys of the cutoff bin -> ties (with their owner thread)
+  if (gathered) {
+    for (int sb = 0; sb < nsb; ++sb) {
+      const int nb = stage_block(sb * SB);
+      for_run(nb, [&](int, uint32_t kk) {
+        if ((kk >> 22) == cb) {
+          const uint32_t slot = atomicAdd(&s_nties, 1u);
+          ties[slot] = kk;
+          owner[slot] = (uint16_t)(sb * SEL_THREADS + threadIdx.x);
         }
-        s_prefix = pre | ((uint32_t)bin << shift);
-        s_need = need - acc;  // how many of the keys equal to the final threshold to take
-      }
+      });
     }
     __syncthreads();
   }
-  const uint32_t thr = s_prefix, take_eq = s_need;
-  // ordered compaction: thread t owns the contiguous run [t*RL, (t+1)*RL)
-  const int RL = (cnt + SEL_THREADS - 1) / SEL_THREADS;
-  const int r0 = threadIdx.x * RL, r1 = min(cnt, r0 + RL);
-  uint32_t n_gt = 0, n_eq = 0;
-  for (int j = r0; j < r1; ++j) {
-    const uint32_t kk = key_at(j);
-    n_gt += kk > thr;
-    n_eq += kk == thr;
-  }
-  uint32_t tot_eq, tot_gt;
-  const uint32_t eq_before = sel_excl_scan(n_eq, scan_sm, tot_eq);
-  // selected before this run: all greater keys before + the equal keys before that are taken
-  const uint32_t gt_before = sel_excl_scan(n_gt, scan_sm, tot_gt);
-  uint32_t pos = gt_before + min(eq_before, take_eq);
-  uint32_t eq_rank = eq_before;
-  for (int j = r0; j < r1; ++j) {
-    const uint32_t kk = key_at(j);
-    bool take = kk > thr;
-    if (kk == thr) {
-      take = eq_rank < take_eq;
-      ++eq_rank;
+  // ---- passes 2, 3: refine the low 22 bits inside the cutoff bin
+#pragma unroll 1
+  for (int d = 0; d < 2; ++d) {
+    const int sh = d == 0 ? 11 : 0;
+    const uint32_t hi_mask = 0xffffffffu << (sh + 11);
+    for (int i = threadIdx.x; i < HIST2; i += SEL_THREADS) hist[i] = 0;
+    __syncthreads();
+    if (gathered) {
+      for (int j = threadIdx.x; j < (int)nbin; j += SEL_THREADS) {
+        const uint32_t kk = ties[j];
+        if ((kk & hi_mask) == prefix) atomicAdd(&hist[(kk >> sh) & (HIST2 - 1)], 1u);
+      }
+    } else {
+      for (int j = threadIdx.x; j < cnt; j += SEL_THREADS) {
+        const uint32_t kk = okey(__ldcg(sc + j));
+        if ((kk & hi_mask) == prefix) atomicAdd(&hist[(kk >> sh) & (HIST2 - 1)], 1u);
+      }
     }
-    if (take) out[pos++] = s0 + j;
+    __syncthreads();
+    find_cut<SEL_THREADS>(hist, HIST2, need, scan_sm, &s_bin, &s_need);
+    prefix |= (uint32_t)s_bin << sh;
+    need = s_need;
+    __syncthreads();
+  }
+  const uint32_t thr = prefix, take_eq = need;
+  // ---- runs pass 2: ordered compaction, super-block by super-block
+  uint32_t base_out = 0, eq_seen = 0;
+  for (int sb = 0; sb < nsb; ++sb) {
+    const int nb = (nsb > 1 || !gathered) ? stage_block(sb * SB) : min(SB, cnt);
+    uint32_t n_gt = 0, n_eq = 0;
+    if (gathered) {
+      // counts of this super-block's runs from the tie list: keys above the cutoff bin are
+      // all selected, inside it the ones > thr (and the first take_eq of those == thr)
+      n_gt_sm[threadIdx.x] = 0;
+      n_eq_sm[threadIdx.x] = 0;
+      __syncthreads();
+      for (int j = threadIdx.x; j < (int)nbin; j += SEL_THREADS) {
+        const int o = owner[j] - sb * SEL_THREADS;
+        if (o >= 0 && o < SEL_THREADS) {
+          if (ties[j] > thr) atomicAdd(&n_gt_sm[o], 1u);
+          else if (ties[j] == thr) atomicAdd(&n_eq_sm[o], 1u);
+        }
+      }
+      __syncthreads();
+      for_run(nb, [&](int, uint32_t kk) { n_gt += (kk >> 22) > cb; });
+      n_gt += n_gt_sm[threadIdx.x];
+      n_eq = n_eq_sm[threadIdx.x];
+    } else {
+      for_run(nb, [&](int, uint32_t kk) {
+        n_gt += kk > thr;
+        n_eq += kk == thr;
+      });
+    }
+    uint32_t tot_eq, tot_gt;
+    const uint32_t eq_before = eq_seen + block_excl_scan<SEL_THREADS>(n_eq, scan_sm, tot_eq);
+    const uint32_t gt_before = block_excl_scan<SEL_THREADS>(n_gt, scan_sm, tot_gt);
+    uint32_t pos = base_out + gt_before + min(eq_before, take_eq) - min(eq_seen, take_eq);
+    uint32_t eq_rank = eq_before;
+    const int base = s0 + sb * SB;
+    for_run(nb, [&](int k, uint32_t kk) {
+      const bool eq = kk == thr;
+      const bool take = kk > thr || (eq && eq_rank < take_eq);
+      eq_rank += eq;
+      if (take) out[pos++] = base + k;
+    });
+    base_out += tot_gt + min(eq_seen + tot_eq, take_eq) - min(eq_seen, take_eq);
+    eq_seen += tot_eq;
   }
 }
 
 }  // namespace pq
 
 static size_t pq_align(size_t x) { return (x + 255) & ~size_t(255); }
+static int pq_score_stride(int maxL) { return (maxL + 3) & ~3; }
 static size_t pq_ws(int B, int Hkv, int maxL) {
   const size_t units = (size_t)B * Hkv;
-  return pq_align(units * pq::M * pq::NC * 4) + pq_align(units * (size_t)maxL * 4);
+  return pq_align(units * pq::M * pq::NC * 4) + pq_align(units * pq::HIST1 * 4) +
+         pq_align(units * (size_t)pq_score_stride(maxL) * 4);
 }
 
 }  // namespace md
@@ -426,8 +588,13 @@ extern "C" MD_API md_status md_pq_select(const void* q, int32_t batch, int32_t n
   MD_REQUIRE(workspace != nullptr && workspace_bytes >= need, MD_ERR_WORKSPACE,
              "md_pq_select: workspace of %zu bytes required, %zu given", need, workspace_bytes);
   const int units = batch * num_kv_heads;
-  auto* lutq = static_cast<int32_t*>(workspace);
-  auto* scores = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(workspace) + pq_align((size_t)units * pq::M * pq::NC * 4));
+  uint8_t* w8 = static_cast<uint8_t*>(workspace);
+  auto* lutq = reinterpret_cast<int32_t*>(w8);
+  w8 += pq_align((size_t)units * pq::M * pq::NC * 4);
+  auto* hist = reinterpret_cast<uint32_t*>(w8);
+  w8 += pq_align((size_t)units * pq::HIST1 * 4);
+  auto* scores = reinterpret_cast<int32_t*>(w8);
+  const int sstride = pq_score_stride(max_kv_len);
   const auto* qq = static_cast<const uint16_t*>(q);
   const auto* cb = static_cast<const uint16_t*>(codebook);
   cudaStream_t s = (cudaStream_t)stream;
@@ -435,34 +602,29 @@ extern "C" MD_API md_status md_pq_select(const void* q, int32_t batch, int32_t n
   const size_t lut_smem = (size_t)g * head_dim * 4;
   if (head_dim == 128)
     launch_pdl(pq::pq_lut_kernel<8>, dim3(units), dim3(256), lut_smem, s, qq, (int)num_q_heads, (int)num_kv_heads,
-               cb, lutq);
+               cb, lutq, hist);
   else
     launch_pdl(pq::pq_lut_kernel<4>, dim3(units), dim3(256), lut_smem, s, qq, (int)num_q_heads, (int)num_kv_heads,
-               cb, lutq);
+               cb, lutq, hist);
   if (md_status st = check_launch("pq_lut_kernel"); st != MD_OK) return st;
-  const unsigned chunks = (unsigned)((max_kv_len + pq::SCORE_CH - 1) / pq::SCORE_CH);
-  launch_pdl(pq::pq_score_kernel, dim3(units, chunks), dim3(pq::SCORE_THREADS), 0, s, codes, (int)code_capacity,
-             (const int32_t*)lutq, kv_len, (int)num_kv_heads, (int)sink, (int)window, scores, (int)max_kv_len);
-  if (md_status st = check_launch("pq_score_kernel"); st != MD_OK) return st;
-  if (max_kv_len <= pq::SEL_SMEM_MAX) {
-    static int done_dev = -1;  // per-process; the attribute call is idempotent (benign race)
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (done_dev != dev) {
-      const size_t smem = (size_t)(pq::SEL_SMEM_MAX + pq::SEL_SMEM_MAX / 32 + 1) * 4;
-      if (cudaFuncSetAttribute(pq::pq_select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess)
-        return check_launch("cudaFuncSetAttribute");
-      done_dev = dev;
-    }
-    const size_t use = (size_t)(max_kv_len + max_kv_len / 32 + 1) * 4;
-    launch_pdl(pq::pq_select_kernel<true>, dim3(units), dim3(pq::SEL_THREADS), use, s, (const int32_t*)scores,
-               (int)max_kv_len, kv_len, (int)num_kv_heads, (int)sink, (int)window, (int)budget, idx, (int)idx_stride,
-               idx_count, tail_start);
-  } else {
-    launch_pdl(pq::pq_select_kernel<false>, dim3(units), dim3(pq::SEL_THREADS), 0, s, (const int32_t*)scores,
-               (int)max_kv_len, kv_len, (int)num_kv_heads, (int)sink, (int)window, (int)budget, idx, (int)idx_stride,
-               idx_count, tail_start);
+  static int done_dev = -1;  // per-process; the attribute call is idempotent (benign race)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done_dev != dev) {
+    if (cudaFuncSetAttribute(pq::pq_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pq::SCORE_SMEM) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(pq::pq_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pq::SEL_SMEM) !=
+            cudaSuccess)
+      return check_launch("cudaFuncSetAttribute");
+    done_dev = dev;
   }
+  const unsigned chunks = (unsigned)((max_kv_len + pq::SCORE_CH - 1) / pq::SCORE_CH);
+  launch_pdl(pq::pq_score_kernel, dim3(units, chunks), dim3(pq::SCORE_THREADS), (size_t)pq::SCORE_SMEM, s, codes,
+             (int)code_capacity, (const int32_t*)lutq, kv_len, (int)num_kv_heads, (int)sink, (int)window, scores,
+             sstride, hist);
+  if (md_status st = check_launch("pq_score_kernel"); st != MD_OK) return st;
+  launch_pdl(pq::pq_select_kernel, dim3(units), dim3(pq::SEL_THREADS), (size_t)pq::SEL_SMEM, s, (const int32_t*)scores, sstride,
+             (const uint32_t*)hist, kv_len, (int)num_kv_heads, (int)sink, (int)window, (int)budget, idx,
+             (int)idx_stride, idx_count, tail_start);
   return check_launch("pq_select_kernel");
 }
