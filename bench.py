@@ -443,7 +443,7 @@ def run_gpu(args):
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "hbm", "achieved": round(v_gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(v_gbs / peak, 4), "traffic": traffic,
-                         "kernel": "md_verify_attn_full (attn_rows_kernel, stream-K persistent, fused split merge)",
+                         "kernel": "md_verify_attn_full (attn_tc_kernel: tcgen05 MMAs with TMEM accumulators, stream-K persistent, fused split merge)",
                          "algorithmic_bytes_per_launch": vb, "ms_per_launch": round(v_ms, 4),
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
             "verify_gbs": round(v_gbs, 1),

@@ -1257,10 +1257,21 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   }
 }
 
+#include "attn_tc.cuh"
+
 // ------------------------------------------------------------------------------ host side
 constexpr int ROWS_CTAS_PER_SM = 2;
 
 static bool use_keys_kernel(int R) { return R <= 8; }
+
+// tcgen05 verify kernel for 8 < R <= 48 at head_dim 128 (MD_TC=0: the mma.sync rows kernel)
+static bool use_tc_kernel(int R, int D, int mode) {
+  static const int on = [] {
+    const char* e = getenv("MD_TC");
+    return (e && atoi(e) == 0) ? 0 : 1;
+  }();
+  return on && D == 128 && mode == 0 /*MODE_VERIFY*/ && R > 8 && R <= 48;
+}
 
 // keys kernel residency: 1 CTA / SM with a deep ring, or 2 CTAs / SM with 2 stages each
 // (tuning knob MD_KEYS_CTAS=1|2 for experiments; default 2)
@@ -1287,7 +1298,8 @@ static int fused_merge_enabled() {
 }
 
 // Persistent stream-K grid: the resident CTAs of one wave.
-static int grid_for(int R, int sm_count) {
+static int grid_for(int R, int sm_count, bool tc = false) {
+  if (tc) return sm_count;
   return sm_count * (use_keys_kernel(R) ? keys_ctas_per_sm() : ROWS_CTAS_PER_SM);
 }
 
@@ -1407,6 +1419,33 @@ static md_status launch_keys(const TmapSet& tm, const AttnParams& p, int grid, c
   return check_launch("attn_keys_kernel");
 }
 
+template <int NP>
+static md_status launch_tc(const TmapSet& tm, const CUtensorMap& qm, const AttnParams& p, int grid, cudaStream_t s) {
+  auto kern = tc::attn_tc_kernel<NP>;
+  constexpr int smem = tc::Cfg<NP>::SMEM;
+  static int done = -1;
+  md_status st = set_smem(kern, smem, &done);
+  if (st != MD_OK) return st;
+  if (launch_pdl(kern, grid, tc::THREADS, smem, s, tm, qm, p) != cudaSuccess) return check_launch("attn_tc_kernel");
+  return check_launch("attn_tc_kernel");
+}
+
+// Q [B][T][Hq][d] as a 4-D map (d, Hq, T, B) with a (64, g, T, 1) box: one box holds the R
+// query rows of a (b, kv head) unit for one 64-column slab, in row order r = t * g + h.
+static md_status make_qmap(CUtensorMap* m, const void* q, int B, int T, int Hq, int g, int d) {
+  auto enc = get_encode();
+  MD_REQUIRE(enc != nullptr, MD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)Hq, (cuuint64_t)T, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)d * 2, (cuuint64_t)Hq * d * 2, (cuuint64_t)T * Hq * d * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)g, (cuuint32_t)T, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(q), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MD_REQUIRE(r == CUDA_SUCCESS, MD_ERR_INVALID_ARG, "cuTensorMapEncodeTiled (q) failed (code %d)", (int)r);
+  return MD_OK;
+}
+
 template <int D>
 static md_status launch_dim(const TmapSet& tm, const AttnParams& p, int grid, cudaStream_t s) {
   if (use_keys_kernel(p.R))
@@ -1457,7 +1496,8 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   const int units = c->batch * c->num_kv_heads;
   MD_REQUIRE(units <= MAX_UNITS, MD_ERR_UNSUPPORTED, "%s: batch * num_kv_heads = %d > %d is not supported", who,
              units, MAX_UNITS);
-  const int grid = grid_for(R, device_sm_count());
+  const bool tcg = use_tc_kernel(R, c->head_dim, mode);
+  const int grid = grid_for(R, device_sm_count(), tcg);
   const size_t need = workspace_for(grid, units, R, c->head_dim);
   MD_REQUIRE(ws != nullptr && ws_bytes >= need, MD_ERR_WORKSPACE, "%s: workspace of %zu bytes required, %zu given",
              who, need, ws_bytes);
@@ -1514,7 +1554,15 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.ws_lse = reinterpret_cast<float*>(w);
   w += align256(chunks * 2 * R * 4);
   p.ws_x = use_keys_kernel(R) ? nullptr : reinterpret_cast<float*>(w);
-  st = (c->head_dim == 128) ? launch_dim<128>(tm, p, grid, s) : launch_dim<64>(tm, p, grid, s);
+  if (tcg) {
+    p.dyn_k = 0;  // static stream-K only
+    CUtensorMap qm;
+    if ((st = make_qmap(&qm, q, c->batch, T, Hq, g, c->head_dim)) != MD_OK) return st;
+    st = (R <= 16) ? launch_tc<16>(tm, qm, p, grid, s) : (R <= 32) ? launch_tc<32>(tm, qm, p, grid, s)
+                                                                   : launch_tc<48>(tm, qm, p, grid, s);
+  } else {
+    st = (c->head_dim == 128) ? launch_dim<128>(tm, p, grid, s) : launch_dim<64>(tm, p, grid, s);
+  }
   if (st != MD_OK || p.fused_merge) return st;
   if (c->head_dim == 128)
     launch_pdl(attn_merge_kernel<128>, dim3(units), dim3(128), 0, s, p, grid);
