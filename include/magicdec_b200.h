@@ -284,6 +284,53 @@ MD_API md_status md_pq_select(const void* q, int32_t batch, int32_t num_q_heads,
                               int32_t* tail_start, void* workspace, size_t workspace_bytes, md_stream_t stream);
 
 /*
+ * Fused tensor-parallel output exchange (the paper runs 8-way tensor
+ * parallelism).  Rank r of `world` owns KV heads [r*Hkv, (r+1)*Hkv) and their
+ * query heads [r*Hq, (r+1)*Hq) (Hkv, Hq = this rank's counts).  Instead of writing a local
+ * output and all-gathering it, the _tp calls store each finished output row into EVERY rank's
+ * full-head buffer (peer-mapped device memory reachable over NVLink / NVSwitch, e.g. CUDA IPC
+ * or symmetric-memory mappings): row (b, t, r*Hq + h) of [B][T][world*Hq][head_dim] fp32.
+ * md_tp_barrier then publishes completion; after it returns on a rank's stream, that rank's
+ * buffer holds every rank's heads.
+ *   out_peers: device array [world] of device pointers, out_peers[k] = rank k's full-head
+ *              buffer (16-byte aligned; out_peers[rank] is this rank's own);
+ *   lse:       local layout [B][T][Hq] (may be NULL), as the non-TP calls.
+ * All other arguments and the workspace are those of md_verify_attn_full / md_draft_attn_sparse
+ * with the rank-local Hq and cache.  Returns MD_ERR_INVALID_ARG for a bad md_tp_out.
+ */
+typedef struct {
+  float* const* out_peers;
+  int32_t world, rank;
+} md_tp_out;
+
+MD_API md_status md_verify_attn_full_tp(const md_kv_cache* cache, const void* q, int32_t num_q_heads, int32_t T,
+                                        const int32_t* kv_len, int32_t max_kv_len, float scale, const md_tp_out* tp,
+                                        float* lse, void* workspace, size_t workspace_bytes, md_stream_t stream);
+MD_API md_status md_draft_attn_sparse_tp(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                         const int32_t* kv_len, int32_t sink, int32_t window, float scale,
+                                         const md_tp_out* tp, float* lse, void* workspace, size_t workspace_bytes,
+                                         md_stream_t stream);
+
+/*
+ * md_tp_barrier — completion barrier of the fused exchange: every rank calls it once after each
+ * _tp attention call, in the same order.  A device-side epoch (uint64 per rank, zero
+ * initialised, bumped by the call itself, so a whole step can be captured in a CUDA graph) is
+ * written with system-scope release into flags[k][rank] of every rank k after a system fence
+ * (ordering the preceding kernels' peer stores); the call then waits (acquire) until
+ * flags[rank][j] reaches the epoch for every j.
+ *   flags_peers: device array [world] of device pointers to each rank's uint64 flags[world]
+ *                (zero initialised, peer-mapped); epoch: this rank's device uint64 counter.
+ * A peer that never arrives traps the kernel after ~20 s (no silent hang).  world <= 32.
+ */
+typedef struct {
+  uint64_t* const* flags_peers;
+  uint64_t* epoch;
+  int32_t world, rank;
+} md_tp_sync;
+
+MD_API md_status md_tp_barrier(const md_tp_sync* sync, md_stream_t stream);
+
+/*
  * md_philox_u32 — Philox4x32-10 uniforms for md_spec_accept (
  * SPEC.md S:472 counter-based PRNG with per-sequence streams; reading Z8).
  * out[b][w] = word (w % 4) of Philox4x32-10(counter = (b, step_lo, step_hi, w / 4),
@@ -292,6 +339,11 @@ MD_API md_status md_pq_select(const void* q, int32_t batch, int32_t num_q_heads,
  */
 MD_API md_status md_philox_u32(uint64_t seed, uint64_t step, int32_t B, int32_t words_per_seq, uint32_t* out,
                         md_stream_t stream);
+/* md_philox_u32_dev — as md_philox_u32 with the step read from device memory (*step, uint64),
+ * so a captured CUDA graph of a whole speculation step draws fresh uniforms at every replay
+ * (the caller advances *step inside the graph). */
+MD_API md_status md_philox_u32_dev(uint64_t seed, const uint64_t* step, int32_t B, int32_t words_per_seq,
+                                   uint32_t* out, md_stream_t stream);
 
 /*
  * md_spec_accept — batched speculative-sampling acceptance (the rule of Leviathan et

@@ -29,7 +29,8 @@ ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_works
                "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed", "md_snapkv_workspace_bytes",
                "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace",
                "md_verify_attn_tree", "md_spec_accept_tree", "md_kv_compact", "md_pq_encode", "md_pq_workspace_bytes",
-               "md_pq_select")
+               "md_pq_select", "md_verify_attn_full_tp", "md_draft_attn_sparse_tp", "md_tp_barrier",
+               "md_philox_u32_dev")
 
 
 class MDError(RuntimeError):
@@ -44,6 +45,17 @@ class KVCache(ctypes.Structure):
                 ("batch", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("capacity", ctypes.c_int32),
                 ("stride_b", ctypes.c_int64), ("stride_h", ctypes.c_int64), ("stride_s", ctypes.c_int64)]
+
+
+class TPOut(ctypes.Structure):
+    """md_tp_out: device array of every rank's full-head output buffer + (world, rank)."""
+    _fields_ = [("out_peers", ctypes.c_void_p), ("world", ctypes.c_int32), ("rank", ctypes.c_int32)]
+
+
+class TPSync(ctypes.Structure):
+    """md_tp_sync: device array of every rank's uint64 flags[world], this rank's epoch counter."""
+    _fields_ = [("flags_peers", ctypes.c_void_p), ("epoch", ctypes.c_void_p), ("world", ctypes.c_int32),
+                ("rank", ctypes.c_int32)]
 
 
 _lib = None
@@ -85,6 +97,13 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.md_spec_accept_tree.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, i32, i32, i32,
                                         ctypes.c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
     lib.md_kv_compact.argtypes = [pc, c_void_p, c_void_p, i32, c_void_p, c_void_p]
+    ptp, psync = ctypes.POINTER(TPOut), ctypes.POINTER(TPSync)
+    lib.md_verify_attn_full_tp.argtypes = [pc, c_void_p, i32, i32, c_void_p, i32, f32, ptp, c_void_p, c_void_p, sz,
+                                           c_void_p]
+    lib.md_draft_attn_sparse_tp.argtypes = [pc, c_void_p, i32, c_void_p, i32, i32, f32, ptp, c_void_p, c_void_p, sz,
+                                            c_void_p]
+    lib.md_tp_barrier.argtypes = [psync, c_void_p]
+    lib.md_philox_u32_dev.argtypes = [u64, c_void_p, i32, i32, c_void_p, c_void_p]
     lib.md_pq_encode.argtypes = [pc, c_void_p, c_void_p, i32, c_void_p, i32, c_void_p]
     lib.md_pq_workspace_bytes.argtypes = [i32, i32, i32]
     lib.md_pq_workspace_bytes.restype = sz
@@ -92,7 +111,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                  c_void_p, i32, c_void_p, c_void_p, c_void_p, sz, c_void_p]
     for name in ("md_kv_append", "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed",
                  "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace", "md_verify_attn_tree",
-                 "md_spec_accept_tree", "md_kv_compact", "md_pq_encode", "md_pq_select"):
+                 "md_spec_accept_tree", "md_kv_compact", "md_pq_encode", "md_pq_select", "md_verify_attn_full_tp",
+                 "md_draft_attn_sparse_tp", "md_tp_barrier", "md_philox_u32_dev"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -235,6 +255,46 @@ def pq_select(q, codebook, codes, kv_len, max_kv_len, sink, window, budget, idx,
     _check(lib.md_pq_select(_ptr(q), B, Hq, Hkv, d, _ptr(codebook), _ptr(codes), codes.shape[2], _ptr(kv_len),
                             int(max_kv_len), int(sink), int(window), int(budget), _ptr(idx), idx.shape[2],
                             _ptr(idx_count), _ptr(tail_start), ws, wsb, _stream(stream)))
+
+
+def tp_out(out_peers_dev, world, rank) -> TPOut:
+    """md_tp_out from an int64 CUDA tensor of device pointers (every rank's full-head buffer)."""
+    return TPOut(_ptr(out_peers_dev), int(world), int(rank))
+
+
+def tp_sync(flags_peers_dev, epoch_dev, world, rank) -> TPSync:
+    return TPSync(_ptr(flags_peers_dev), _ptr(epoch_dev), int(world), int(rank))
+
+
+def verify_attn_full_tp(q, k_cache, v_cache, kv_len, max_kv_len, scale, tp, lse=None, workspace=None, stream=None):
+    """Rank-local verify whose outputs land in every rank's [B, T, world*Hq, d] buffer (tp: TPOut)."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_verify_attn_full_tp(ctypes.byref(c), _ptr(q), q.shape[2], q.shape[1], _ptr(kv_len),
+                                      int(max_kv_len), float(scale), ctypes.byref(tp), _ptr(lse), ws, wsb,
+                                      _stream(stream)))
+
+
+def draft_attn_sparse_tp(q, k_cache, v_cache, kv_len, sink, window, scale, tp, lse=None, workspace=None, stream=None):
+    """Rank-local StreamingLLM draft whose outputs land in every rank's [B, world*Hq, d] buffer."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_draft_attn_sparse_tp(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(kv_len), int(sink), int(window),
+                                       float(scale), ctypes.byref(tp), _ptr(lse), ws, wsb, _stream(stream)))
+
+
+def tp_barrier(sync, stream=None):
+    """Completion barrier of the fused exchange (sync: TPSync)."""
+    _check(load_library().md_tp_barrier(ctypes.byref(sync), _stream(stream)))
+
+
+def philox_u32_dev(seed, step_dev, out, stream=None):
+    """As philox_u32 with the step read from a device uint64 (int64 tensor of one element)."""
+    lib = load_library()
+    _check(lib.md_philox_u32_dev(int(seed) & (2**64 - 1), _ptr(step_dev), out.shape[0], out.shape[1], _ptr(out),
+                                 _stream(stream)))
 
 
 def philox_u32(seed, step, out, stream=None):

@@ -76,6 +76,11 @@ struct AttnParams {
   int dyn_static_permille;  // share of the tiles assigned statically (per mille)
   int dyn_min_tiles;      // dynamic only when total tiles >= dyn_min_tiles * active CTAs
   const uint32_t* tree_mask;  // verify: [B][T] bit j of (b, t) = node t sees new key n-T+j (null: causal chain)
+  // outputs: row o_row(b, kvh, r) of [B][T][out_hq][D]; with tensor parallelism (f1) every
+  // rank's full-head buffer out_peers[0..tp_world) receives this rank's heads at head offset
+  // out_h0 (stores over NVLink to peer-mapped memory), otherwise only `out`
+  float* const* out_peers;
+  int tp_world, out_hq, out_h0;
   int mode;
   float scale_log2;       // scale * log2(e)
 };
@@ -295,6 +300,22 @@ __device__ __forceinline__ void trace_stamp(const AttnParams& p, int k) {
 __device__ __forceinline__ int64_t out_row(const AttnParams& p, int b, int kvh, int r) {
   return (int64_t)(b * p.T + r / p.g) * p.Hq + kvh * p.g + r % p.g;
 }
+// row of query row r of unit (b, kvh) in the output layout (local heads, or the TP full-head layout)
+__device__ __forceinline__ int64_t o_row(const AttnParams& p, int b, int kvh, int r) {
+  return (int64_t)(b * p.T + r / p.g) * p.out_hq + p.out_h0 + kvh * p.g + r % p.g;
+}
+// final output store: local buffer, or every TP rank's buffer (f1: the all-gather is the store)
+template <typename V>
+__device__ __forceinline__ void store_out(const AttnParams& p, int64_t off, V v) {
+  if (p.out_peers == nullptr) {
+    *reinterpret_cast<V*>(p.out + off) = v;
+    return;
+  }
+  for (int k = 0; k < p.tp_world; ++k) {
+    float* base = reinterpret_cast<float*>(__ldg(reinterpret_cast<const unsigned long long*>(p.out_peers) + k));
+    *reinterpret_cast<V*>(base + off) = v;
+  }
+}
 
 // ------------------------------------------------------------------ producer
 // Stream the K/V tiles of one segment into the ring; `it` is the running tile counter.
@@ -410,9 +431,8 @@ __device__ void finish_unit(const AttnParams& p, const Seg& sg, const Plan& pl, 
       acc.w = acc.w * a + w * v.w;
     }
     const float inv = W > 0.f ? 1.f / W : 0.f;
-    const int64_t orow = out_row(p, sg.b, sg.kvh, r);
-    *reinterpret_cast<float4*>(p.out + orow * D + c4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-    if (c4 == 0 && p.lse != nullptr) p.lse[orow] = (W > 0.f) ? (M + __log2f(W)) * LN2 : -INFINITY;
+    store_out(p, o_row(p, sg.b, sg.kvh, r) * D + c4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+    if (c4 == 0 && p.lse != nullptr) p.lse[out_row(p, sg.b, sg.kvh, r)] = (W > 0.f) ? (M + __log2f(W)) * LN2 : -INFINITY;
   }
 }
 
@@ -459,9 +479,8 @@ __global__ void __launch_bounds__(128) attn_merge_kernel(const AttnParams p, int
       acc.w += w * v.w;
     }
     const float inv = W > 0.f ? 1.f / W : 0.f;
-    const int64_t orow = out_row(p, b, kvh, r);
-    *reinterpret_cast<float4*>(p.out + orow * D + c4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-    if (c4 == 0 && p.lse != nullptr) p.lse[orow] = (W > 0.f) ? (M + __log2f(W)) * LN2 : -INFINITY;
+    store_out(p, o_row(p, b, kvh, r) * D + c4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+    if (c4 == 0 && p.lse != nullptr) p.lse[out_row(p, b, kvh, r)] = (W > 0.f) ? (M + __log2f(W)) * LN2 : -INFINITY;
   }
 }
 
@@ -818,19 +837,19 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
       for (int h = 0; h < 2; ++h) {
         const int r = mt * 16 + gq + h * 8;
         if (r < p.R) {
-          float* dst;
           if (complete) {
-            const int64_t orow = out_row(p, b, kvh, r);
-            dst = p.out + orow * D;
-            if (cq == 0 && p.lse != nullptr) p.lse[orow] = lsebuf[r] * LN2;
+            const int64_t orow = o_row(p, b, kvh, r) * D;
+            if (cq == 0 && p.lse != nullptr) p.lse[out_row(p, b, kvh, r)] = lsebuf[r] * LN2;
+#pragma unroll
+            for (int i = 0; i < NT_O; ++i) store_out(p, orow + i * 8 + cq * 2, make_float2(o[i][2 * h], o[i][2 * h + 1]));
           } else {
             const int64_t prow = (int64_t)slot_base * p.R + r;
-            dst = p.ws_o + prow * D;
+            float* dst = p.ws_o + prow * D;
             if (cq == 0) __stcg(p.ws_lse + prow, lsebuf[r]);
-          }
 #pragma unroll
-          for (int i = 0; i < NT_O; ++i)
-            __stcg(reinterpret_cast<float2*>(dst + i * 8 + cq * 2), make_float2(o[i][2 * h], o[i][2 * h + 1]));
+            for (int i = 0; i < NT_O; ++i)
+              __stcg(reinterpret_cast<float2*>(dst + i * 8 + cq * 2), make_float2(o[i][2 * h], o[i][2 * h + 1]));
+          }
         }
       }
     }
@@ -1229,9 +1248,8 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         const float4 c = *reinterpret_cast<const float4*>(obuf + FRAG + r * D + sc);
         const float4 v = make_float4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
         if (complete) {
-          const int64_t orow = out_row(p, sg.b, sg.kvh, r);
-          *reinterpret_cast<float4*>(p.out + orow * D + c4) = v;
-          if (c4 == 0 && p.lse != nullptr) p.lse[orow] = lsebuf[r] * LN2;
+          store_out(p, o_row(p, sg.b, sg.kvh, r) * D + c4, v);
+          if (c4 == 0 && p.lse != nullptr) p.lse[out_row(p, sg.b, sg.kvh, r)] = lsebuf[r] * LN2;
         } else {
           const int64_t prow = (int64_t)slot_base * p.R + r;
           __stcg(reinterpret_cast<float4*>(p.ws_o + prow * D + c4), v);
@@ -1479,6 +1497,7 @@ struct IndexedArgs {
   const int32_t* idx_count = nullptr;
   const int32_t* tail_start = nullptr;
   const uint32_t* tree_mask = nullptr;  // verify only
+  const md_tp_out* tp = nullptr;        // f1: outputs stored into every TP rank's full-head buffer
 };
 
 static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int T, const int32_t* kv_len, int sink,
@@ -1486,6 +1505,12 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
                                cudaStream_t s, const char* who, const IndexedArgs& ix = IndexedArgs()) {
   md_status st = check_cache(c, who);
   if (st != MD_OK) return st;
+  if (ix.tp != nullptr) {
+    MD_REQUIRE(ix.tp->out_peers != nullptr && ix.tp->world >= 1 && ix.tp->rank >= 0 && ix.tp->rank < ix.tp->world &&
+                   ix.tp->world <= 64,
+               MD_ERR_INVALID_ARG, "%s: bad md_tp_out (need out_peers, 0 <= rank < world <= 64)", who);
+    out = reinterpret_cast<float*>(16);  // unused: every output row goes to out_peers
+  }
   MD_REQUIRE(q != nullptr && kv_len != nullptr && out != nullptr, MD_ERR_INVALID_ARG, "%s: NULL q/kv_len/out", who);
   MD_REQUIRE(Hq >= 1 && Hq % c->num_kv_heads == 0, MD_ERR_INVALID_ARG, "%s: num_q_heads must be a multiple of Hkv",
              who);
@@ -1536,6 +1561,10 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.idx_count = ix.idx_count;
   p.tail_start = ix.tail_start;
   p.tree_mask = ix.tree_mask;
+  p.out_peers = ix.tp ? ix.tp->out_peers : nullptr;
+  p.tp_world = ix.tp ? ix.tp->world : 1;
+  p.out_hq = ix.tp ? ix.tp->world * Hq : Hq;
+  p.out_h0 = ix.tp ? ix.tp->rank * Hq : 0;
   p.trace = (g_trace != nullptr && g_trace_bytes >= (size_t)grid * TRACE_SLOTS * 8) ? g_trace : nullptr;
   p.fused_merge = fused_merge_enabled();
   p.row_sB = c->stride_b / c->head_dim;
@@ -1644,6 +1673,37 @@ extern "C" md_status md_draft_attn_indexed(const md_kv_cache* cache, const void*
   ix.tail_start = tail_start;
   return run_attention(cache, q, num_q_heads, 1, kv_len, 0, 0, MODE_INDEXED, scale, out, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_draft_attn_indexed", ix);
+}
+
+extern "C" md_status md_verify_attn_full_tp(const md_kv_cache* cache, const void* q, int32_t num_q_heads, int32_t T,
+                                            const int32_t* kv_len, int32_t max_kv_len, float scale,
+                                            const md_tp_out* tp, float* lse, void* workspace, size_t workspace_bytes,
+                                            md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(T >= 1 && T <= 16, MD_ERR_UNSUPPORTED, "md_verify_attn_full_tp: T must be in [1, 16]");
+  MD_REQUIRE(cache != nullptr && tp != nullptr, MD_ERR_INVALID_ARG, "md_verify_attn_full_tp: NULL cache / tp");
+  MD_REQUIRE(max_kv_len >= T && max_kv_len <= cache->capacity, MD_ERR_INVALID_ARG,
+             "md_verify_attn_full_tp: need T <= max_kv_len <= capacity");
+  IndexedArgs ix;
+  ix.tp = tp;
+  return run_attention(cache, q, num_q_heads, T, kv_len, 0, 0, MODE_VERIFY, scale, nullptr, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_verify_attn_full_tp", ix);
+}
+
+extern "C" md_status md_draft_attn_sparse_tp(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                             const int32_t* kv_len, int32_t sink, int32_t window, float scale,
+                                             const md_tp_out* tp, float* lse, void* workspace, size_t workspace_bytes,
+                                             md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(cache != nullptr && tp != nullptr, MD_ERR_INVALID_ARG, "md_draft_attn_sparse_tp: NULL cache / tp");
+  MD_REQUIRE(sink >= 0 && window >= 0 && (int64_t)sink + window >= 1, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_tp: need sink >= 0, window >= 0, sink + window >= 1");
+  IndexedArgs ix;
+  ix.tp = tp;
+  return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, nullptr, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_tp", ix);
 }
 
 extern "C" MD_API md_status md_debug_trace(void* buf, size_t bytes) {

@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (r < p.R) {
           const float L = crow[r];
           const float val = (L > 0.f) ? o[r] / L : 0.f;
-          if (complete) p.out[out_row(p, b, kvh, r) * D + x] = val;
+          if (complete) store_out(p, o_row(p, b, kvh, r) * D + x, val);
           else __stcg(p.ws_o + ((int64_t)slot_base * p.R + r) * D + x, val);
         }
       }

@@ -38,9 +38,12 @@ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint3
   return Philox4{{c0, c1, c2, c3}};
 }
 
-__global__ void philox_kernel(uint64_t seed, uint64_t step, int B, int words, uint32_t* __restrict__ out) {
+// step_dev != null: the step is read from device memory (graph replays draw fresh words)
+__global__ void philox_kernel(uint64_t seed, uint64_t step, const uint64_t* step_dev, int B, int words,
+                              uint32_t* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
+  if (step_dev != nullptr) step = *step_dev;
   const int blocks_per_seq = (words + 3) / 4;
   const int64_t total = (int64_t)B * blocks_per_seq;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -307,8 +310,23 @@ extern "C" md_status md_philox_u32(uint64_t seed, uint64_t step, int32_t B, int3
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 4096) blocks = 4096;
   launch_pdl(philox_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0, (cudaStream_t)stream, seed, step,
-             (int)B, (int)words_per_seq, out);
+             (const uint64_t*)nullptr, (int)B, (int)words_per_seq, out);
   return check_launch("md_philox_u32");
+}
+
+extern "C" md_status md_philox_u32_dev(uint64_t seed, const uint64_t* step, int32_t B, int32_t words_per_seq,
+                                       uint32_t* out, md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(out != nullptr && step != nullptr, MD_ERR_INVALID_ARG, "md_philox_u32_dev: NULL output / step");
+  MD_REQUIRE(B >= 1 && words_per_seq >= 1, MD_ERR_INVALID_ARG, "md_philox_u32_dev: B and words_per_seq must be >= 1");
+  const int64_t total = (int64_t)B * ((words_per_seq + 3) / 4);
+  const int threads = 256;
+  int64_t blocks = (total + threads - 1) / threads;
+  if (blocks > 4096) blocks = 4096;
+  launch_pdl(philox_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0, (cudaStream_t)stream, seed,
+             (uint64_t)0, step, (int)B, (int)words_per_seq, out);
+  return check_launch("md_philox_u32_dev");
 }
 
 extern "C" md_status md_spec_accept(const float* p, const float* q, const int32_t* draft_tokens, const uint32_t* rnd,
