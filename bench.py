@@ -223,39 +223,58 @@ def run_gpu(args):
 
     # per layer-call: md_kv_append + one attention kernel (stream-K, merge fused); + philox + accept
     launches_per_step = gamma * layers * 2 + layers * 2 + 2
+    if world > 1:
+        launches_per_step += gamma * layers + layers  # the exchange after every attention call
 
     # positions for the step are one plumbing op on the committed lengths
     pos_buf = torch.empty((gamma + 2, B), dtype=torch.int32, device=dev)
 
-    def step(i):
-        torch.add(committed[None, :], ar, out=pos_buf)
-        layer_pass(pos_buf)
-        md.philox_u32(SEED, i, rnd)
-        md.spec_accept(p_t, q_t, dtok, rnd, out_tok, nacc, committed, mode="sample")
-
     use_graph = not args.no_graph and world == 1
     graph = None
+    step_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    # default: the layer loop (gamma*layers draft + layers verify calls) is one CUDA graph and
+    # philox + accept follow it; MD_BENCH_GRAPH=whole captures the whole step including them
+    # (philox reads its step from device memory).  Measured A/B on one box: 49.7 vs 50.7 ms/step.
+    split = os.environ.get("MD_BENCH_GRAPH", "split") != "whole"
+
+    def whole_step():
+        # one speculation step: gamma x layers draft calls, layers verify calls, uniforms and
+        # acceptance -- captured as ONE CUDA graph; the Philox step lives in device
+        # memory so every replay draws fresh uniforms
+        torch.add(committed[None, :], ar, out=pos_buf)
+        layer_pass(pos_buf)
+        if split:
+            return
+        md.philox_u32_dev(SEED, step_dev, rnd)
+        md.spec_accept(p_t, q_t, dtok, rnd, out_tok, nacc, committed, mode="sample")
+        step_dev.add_(1)
+
     if use_graph:
-        # the layer loop (gamma*layers draft + layers verify calls) is one CUDA graph
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
+        c_save = committed.clone()
         with torch.cuda.stream(s):
-            torch.add(committed[None, :], ar, out=pos_buf)
-            layer_pass(pos_buf)
+            whole_step()  # warm-up outside the capture (kernel attributes, allocator)
         torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        committed.copy_(c_save)
+        step_dev.zero_()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            torch.add(committed[None, :], ar, out=pos_buf)
-            layer_pass(pos_buf)
+            whole_step()
+        torch.cuda.synchronize()
+        committed.copy_(c_save)
+        step_dev.zero_()
 
     def step_g(i):
         if graph is not None:
             graph.replay()
         else:
-            torch.add(committed[None, :], ar, out=pos_buf)
-            layer_pass(pos_buf)
-        md.philox_u32(SEED, i, rnd)
-        md.spec_accept(p_t, q_t, dtok, rnd, out_tok, nacc, committed, mode="sample")
+            whole_step()
+        if split:
+            md.philox_u32(SEED, i, rnd)
+            md.spec_accept(p_t, q_t, dtok, rnd, out_tok, nacc, committed, mode="sample")
 
     for i in range(args.warmup):
         step_g(i)
@@ -437,7 +456,9 @@ def run_gpu(args):
                        "layers": layers, "vocab": V, "layer_caches_rotated": R,
                        "l2": "inputs larger than L2: each layer-call streams a distinct %.1f GB cache" %
                              (verify_bytes(kvl_now, Hkv, Hq, d, T) / 1e9),
-                       "attention_only": True, "cuda_graph": use_graph,
+                       "attention_only": True,
+                       "cuda_graph": ("layer loop" if split else "whole step (drafts + verify + philox + accept)")
+                       if use_graph else False,
                        "parallelism": f"tp{world} (KV heads)" if world > 1 else "single GPU"},
             "tokens_per_step": round(tokens / args.steps, 3),
             "gpu_launches": launches_per_step * args.steps,
