@@ -203,6 +203,12 @@ def run_gpu(args):
                        dtype=torch.uint8, device=dev)
     gath_v = torch.empty((world, B, T, Hq, d), device=dev) if world > 1 else None
     gath_d = torch.empty((world, B, Hq, d), device=dev) if world > 1 else None
+    # f1: --tp-exchange p2p replaces the all-gather with peer stores + md_tp_barrier
+    xv = xd = None
+    if world > 1 and args.tp_exchange == "p2p":
+        from paper_2408_11049_b200.tp import PeerExchange
+        xv = PeerExchange((B, T, Hq_full, d))
+        xd = PeerExchange((B, Hq_full, d))
 
     def layer_pass(pos):
         # pos[j] = committed + j  (rows: draft j start = pos[j], draft j kv_len = pos[j+1],
@@ -211,12 +217,20 @@ def run_gpu(args):
             for l in range(layers):
                 kb, vb = kc[l % R], vc[l % R]
                 md.kv_append(kb, vb, knew_d, vnew_d, pos[j])
+                if xd is not None:
+                    md.draft_attn_sparse_tp(qd, kb, vb, pos[j + 1], sink, window, scale, xd.out, lse_d, ws_d)
+                    xd.barrier()
+                    continue
                 md.draft_attn_sparse(qd, kb, vb, pos[j + 1], sink, window, scale, out_d, lse_d, ws_d)
                 if world > 1:
                     gather_rank_major(out_d, gath_d)
         for l in range(layers):
             kb, vb = kc[l % R], vc[l % R]
             md.kv_append(kb, vb, knew_v, vnew_v, pos[0])
+            if xv is not None:
+                md.verify_attn_full_tp(qv, kb, vb, pos[gamma + 1], max_kv, scale, xv.out, lse_v, ws_v)
+                xv.barrier()
+                continue
             md.verify_attn_full(qv, kb, vb, pos[gamma + 1], max_kv, scale, out_v, lse_v, ws_v)
             if world > 1:
                 gather_rank_major(out_v, gath_v)
@@ -459,7 +473,8 @@ def run_gpu(args):
                        "attention_only": True,
                        "cuda_graph": ("layer loop" if split else "whole step (drafts + verify + philox + accept)")
                        if use_graph else False,
-                       "parallelism": f"tp{world} (KV heads)" if world > 1 else "single GPU"},
+                       "parallelism": (f"tp{world} (KV heads, {args.tp_exchange} exchange)" if world > 1
+                                       else "single GPU")},
             "tokens_per_step": round(tokens / args.steps, 3),
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "hbm", "achieved": round(v_gbs, 1), "peak": peak, "unit": "GB/s",
@@ -583,6 +598,8 @@ def main(argv=None):
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-ar", action="store_true")
+    ap.add_argument("--tp-exchange", choices=["nccl", "p2p"], default="nccl",
+                    help="N>1: NCCL all-gather of per-head outputs, or the fused peer-store exchange (f1)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

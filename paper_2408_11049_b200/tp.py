@@ -47,3 +47,36 @@ def gather_heads(out_local: torch.Tensor, world: int, group=None, buf: torch.Ten
     nd = len(shape)
     perm = list(range(1, nd - 1)) + [0, nd - 1, nd]
     return buf.permute(*perm).reshape(*shape[:-2], world * shape[-2], shape[-1])
+
+
+class PeerExchange:
+    """Fused output exchange: a full-head output buffer on every rank,
+    peer-mapped with torch symmetric memory (NVLink / NVSwitch), plus the completion flags of
+    md_tp_barrier.  Rank r's md_*_tp calls store its heads into every rank's buffer; after
+    `barrier()` on a rank's stream its buffer holds all heads (no NCCL all-gather).
+    Host plumbing only: the stores and the barrier are CUDA kernels of the library."""
+
+    def __init__(self, shape, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        import paper_2408_11049_b200 as md
+
+        group = group or dist.group.WORLD
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.buf = symm_mem.empty(tuple(shape), dtype=torch.float32, device=dev)
+        hb = symm_mem.rendezvous(self.buf, group.group_name)
+        self.flags = symm_mem.empty((self.world,), dtype=torch.int64, device=dev)
+        hf = symm_mem.rendezvous(self.flags, group.group_name)
+        self.flags.zero_()
+        self.peers = torch.tensor(list(hb.buffer_ptrs), dtype=torch.int64, device=dev)
+        self.flag_peers = torch.tensor(list(hf.buffer_ptrs), dtype=torch.int64, device=dev)
+        self.epoch = torch.zeros(1, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize()
+        dist.barrier(group)
+        self.out = md.tp_out(self.peers, self.world, self.rank)
+        self.sync = md.tp_sync(self.flag_peers, self.epoch, self.world, self.rank)
+
+    def barrier(self, stream=None):
+        import paper_2408_11049_b200 as md
+        md.tp_barrier(self.sync, stream)
