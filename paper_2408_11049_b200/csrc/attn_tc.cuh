@@ -118,6 +118,10 @@ __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, long long*
 __device__ __forceinline__ int seg_stages(const Ranges& rg) { return (rg.e0 - rg.s0 + KT - 1) / KT; }
 
 // TMA producer (one thread): Q rows of the segment, then its K/V stages
+#ifndef MD_TC_PF
+#define MD_TC_PF 0  // measured: 2 or 4 stages of L2 prefetch slow Llama verify 1.26 -> 1.41 ms
+#endif
+constexpr int PF = MD_TC_PF;  // stages prefetched into L2 ahead of the ring
 template <int NP>
 __device__ void produce(const AttnParams& p, const TmapSet& tm, const CUtensorMap* qmap, const Seg& sg,
                         const Ranges& rg, uint8_t* ring, uint8_t* qbuf, uint64_t* full, uint64_t* empty,
@@ -142,6 +146,19 @@ __device__ void produce(const AttnParams& p, const TmapSet& tm, const CUtensorMa
       else if (hv > 0) bytes += 2 * 2 * ((hv + BOX_ROWS - 1) / BOX_ROWS) * BOX_ROWS * 128;
     }
     mbar_arrive_expect_tx(&full[stage], bytes);
+    // L2 prefetch PF stages ahead (full 64-row boxes only): deepens the memory pipeline beyond
+    // the shared-memory ring, which the consumers hold for a stage's S^T, softmax and PV
+    if (PF > 0) {
+      const int pp = pos + PF * KT;
+      for (int h = 0; h < 2; ++h) {
+        const int r0 = pp + h * TK;
+        if (r0 + TK <= rg.e0)
+          for (int sub = 0; sub < 2; ++sub) {
+            tma_prefetch_4d(&tm.k_full, sub * 64, r0, sg.kvh, sg.b);
+            tma_prefetch_4d(&tm.v_full, sub * 64, r0, sg.kvh, sg.b);
+          }
+      }
+    }
     for (int h = 0; h < 2; ++h) {
       const int hv = nvalid - h * TK, r0 = pos + h * TK;
       for (int sub = 0; sub < 2; ++sub) {
