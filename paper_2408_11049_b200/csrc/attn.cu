@@ -1437,9 +1437,9 @@ static md_status launch_keys(const TmapSet& tm, const AttnParams& p, int grid, c
   return check_launch("attn_keys_kernel");
 }
 
-template <int NP>
+template <int NP, int RR>
 static md_status launch_tc(const TmapSet& tm, const CUtensorMap& qm, const AttnParams& p, int grid, cudaStream_t s) {
-  auto kern = tc::attn_tc_kernel<NP>;
+  auto kern = tc::attn_tc_kernel<NP, RR>;
   constexpr int smem = tc::Cfg<NP>::SMEM;
   static int done = -1;
   md_status st = set_smem(kern, smem, &done);
@@ -1587,8 +1587,12 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
     p.dyn_k = 0;  // static stream-K only
     CUtensorMap qm;
     if ((st = make_qmap(&qm, q, c->batch, T, Hq, g, c->head_dim)) != MD_OK) return st;
-    st = (R <= 16) ? launch_tc<16>(tm, qm, p, grid, s) : (R <= 32) ? launch_tc<32>(tm, qm, p, grid, s)
-                                                                   : launch_tc<48>(tm, qm, p, grid, s);
+    // the BASELINE shapes get a compile-time row count (Llama-3.1 g=4 x T=5, Qwen2.5 g=7 x T=5)
+    st = (R == 20)   ? launch_tc<32, 20>(tm, qm, p, grid, s)
+         : (R == 35) ? launch_tc<48, 35>(tm, qm, p, grid, s)
+         : (R <= 16) ? launch_tc<16, 0>(tm, qm, p, grid, s)
+         : (R <= 32) ? launch_tc<32, 0>(tm, qm, p, grid, s)
+                     : launch_tc<48, 0>(tm, qm, p, grid, s);
   } else {
     st = (c->head_dim == 128) ? launch_dim<128>(tm, p, grid, s) : launch_dim<64>(tm, p, grid, s);
   }

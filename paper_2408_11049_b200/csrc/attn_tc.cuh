@@ -179,10 +179,12 @@ __device__ void produce(const AttnParams& p, const TmapSet& tm, const CUtensorMa
   }
 }
 
-template <int NP>
+// RR > 0: the row count R is a compile-time constant (the hot configurations), else p.R
+template <int NP, int RR>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ CUtensorMap qmap, const AttnParams p) {
   using C = Cfg<NP>;
+  const int R = RR > 0 ? RR : p.R;
   constexpr int NSTAGE = C::NSTAGE, NQ = C::NQ;
   constexpr int D = 128;
   extern __shared__ uint8_t smem_raw[];
@@ -383,18 +385,30 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[sb]);
         TSEC(0)
-        // scale + mask; the causal chain / tree mask among the T new keys only matters in the
-        // unit's last tile (a rare, divergent branch kept out of the unrolled fast path)
+        // x_r = s_r * scale * log2(e) - m_r: one FMA per row, reused for the raise test and
+        // the exponent.  Masking (keys past the valid range; the causal chain / tree mask among
+        // the T new keys) only exists in a unit's last stage: a tile-uniform branch.
         const float sl2 = p.scale_log2;
-#pragma unroll
-        for (int r = 0; r < NP; ++r) v[r] = (valid && r < p.R) ? v[r] * sl2 : -INFINITY;
+        const bool edge = (nvalid < KT) || (pos + KT > vbase);
         const int rel = key - vbase;
-        if (pos + KT > vbase && rel >= 0 && valid) {
-          int t = 0, hh = 0;
+        float xs[NP];
+        float xmax = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < NP; ++r) {
+          xs[r] = (r < R) ? fmaf(v[r], sl2, -mr[r]) : -INFINITY;
+          xmax = fmaxf(xmax, xs[r]);
+        }
+        if (edge) {
+          // masked keys get x = -inf (also their scaled scores v = -inf for a max raise)
           uint32_t msk = p.tree_mask ? __ldg(p.tree_mask + (size_t)b * p.T) : 1u;
+          int t = 0, hh = 0;
+          xmax = -INFINITY;
 #pragma unroll
           for (int r = 0; r < NP; ++r) {
-            if (r < p.R && !((msk >> (rel & 31)) & 1u)) v[r] = -INFINITY;
+            const bool hide = !valid || (rel >= 0 && !((msk >> (rel & 31)) & 1u));
+            if (r < R && hide) xs[r] = -INFINITY;
+            if (r < R && hide) v[r] = -INFINITY;
+            xmax = fmaxf(xmax, xs[r]);
             if (++hh == p.g) {  // next query token t (row r = t * g + hh)
               hh = 0;
               ++t;
@@ -402,9 +416,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
           }
         }
-        bool need = false;
-#pragma unroll
-        for (int r = 0; r < NP; ++r) need |= v[r] > mr[r] + THR;
+        const bool need = xmax > THR;  // some score exceeds its row maximum by > 2^8 (or m = -inf)
         TSEC(1)
         // the previous tile's PV must be complete before P is rewritten or O^T rescaled
         if (tt > 0) twait(pempty, (tt - 1) & 1, wpe);
@@ -413,13 +425,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           // raise every row's maximum to this tile's (or keep it): per-row max over the tile
 #pragma unroll
           for (int r = 0; r < NP; ++r) {
-            float m = v[r];
+            if (r < R) {
+              float m = (v[r] == -INFINITY) ? -INFINITY : v[r] * sl2;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-            if (lane == 0) red[warp * NP + r] = m;
+              for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+              if (lane == 0) red[warp * NP + r] = m;
+            }
           }
           bar128();
-          if (x < NP) {
+          if (x < R) {
             const float m = fmaxf(fmaxf(red[x], red[NP + x]), fmaxf(red[2 * NP + x], red[3 * NP + x]));
             const float mo = mrow[x];
             const float mn = fmaxf(mo, m);
@@ -429,8 +443,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           bar128();
 #pragma unroll
           for (int r = 0; r < NP; ++r) {
-            mr[r] = mrow[r];
-            lacc[r] *= crow[r];
+            if (r < R) {
+              mr[r] = mrow[r];
+              lacc[r] *= crow[r];
+              const float base = (mr[r] == -INFINITY) ? 0.f : mr[r];
+              xs[r] = (v[r] == -INFINITY) ? -INFINITY : fmaf(v[r], sl2, -base);
+            }
           }
           if (j > 0) {  // O^T already holds PV of earlier tiles of this segment: rescale it
             const uint32_t oa = tbase + 2 * NP + ob * NP + lane_off;
@@ -440,20 +458,18 @@ __global__ void __launch_bounds__(THREADS, 1)
               tld16(oa + c, o);
               wait_ld();
 #pragma unroll
-              for (int i = 0; i < 16; ++i) o[i] *= crow[c + i];
+              for (int i = 0; i < 16; ++i) o[i] *= (c + i < R) ? crow[c + i] : 0.f;
               tst16(oa + c, o);
             }
             wait_st();
           }
         }
         TSEC(2)
-        // P = 2^(s - m); row sums accumulate in fp32, the MMA operand is bf16
+        // P = 2^x; row sums accumulate in fp32, the MMA operand is bf16
         uint32_t pk[NP / 2];
 #pragma unroll
         for (int r = 0; r < NP; r += 2) {
-          const float b0 = (mr[r] == -INFINITY) ? 0.f : mr[r];
-          const float b1 = (mr[r + 1] == -INFINITY) ? 0.f : mr[r + 1];
-          const float p0 = ex2(v[r] - b0), p1 = ex2(v[r + 1] - b1);
+          const float p0 = (r < R) ? ex2(xs[r]) : 0.f, p1 = (r + 1 < R) ? ex2(xs[r + 1]) : 0.f;
           lacc[r] += p0;
           lacc[r + 1] += p1;
           pk[r / 2] = pack_bf16(p0, p1);
@@ -503,14 +519,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int slot_base = chunk * 2 + pl.slot(sg.ustart, chunk);
 #pragma unroll
       for (int r = 0; r < NP; ++r) {
-        if (r < p.R) {
+        if (r < R) {
           const float L = crow[r];
           const float val = (L > 0.f) ? o[r] / L : 0.f;
           if (complete) store_out(p, o_row(p, b, kvh, r) * D + x, val);
           else __stcg(p.ws_o + ((int64_t)slot_base * p.R + r) * D + x, val);
         }
       }
-      if (x < p.R) {
+      if (x < R) {
         const float L = crow[x], m = mrow[x];
         const float lse2 = (L > 0.f) ? m + __log2f(L) : -INFINITY;
         if (complete) {
