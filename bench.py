@@ -302,11 +302,16 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
         e0.record()
+        marks = []
         for i in range(args.steps):
             step_g(args.warmup + i)
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            marks.append(ev)
         e1.record()
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    per_step = np.diff([0.0] + [e0.elapsed_time(ev) for ev in marks])
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -466,6 +471,7 @@ def run_gpu(args):
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": round(ms_per_step, 4),
+            "ms_per_step_p10_p50_p90": [round(float(np.percentile(per_step, q)), 3) for q in (10, 50, 90)],
             "higher_is_better": True,
             "scaling": "strong",  # the B=64 workload is split over the N GPUs (KV-head TP)
             "vs_baseline": None,
