@@ -81,6 +81,7 @@ struct AttnParams {
   // out_h0 (stores over NVLink to peer-mapped memory), otherwise only `out`
   float* const* out_peers;
   int tp_world, out_hq, out_h0;
+  int pdl_early;          // tcgen05 kernel: trigger the dependent launch at entry (1) or at exit (0)
   int mode;
   float scale_log2;       // scale * log2(e)
 };
@@ -940,7 +941,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     if ((row % C::ROWS) >= p.R) *reinterpret_cast<uint4*>(qbuf + row * C::QSTR + c * 16) = make_uint4(0, 0, 0, 0);
   }
   trace_stamp(p, 0);
-  pdl_trigger();
+  if (p.pdl_early) pdl_trigger();  // else the dependent launch waits for this grid's exit
   pdl_wait();  // kv_len, the cache and q may come from the previous kernel
   trace_stamp(p, 1);
   __syncthreads();
@@ -1583,8 +1584,12 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.ws_lse = reinterpret_cast<float*>(w);
   w += align256(chunks * 2 * R * 4);
   p.ws_x = use_keys_kernel(R) ? nullptr : reinterpret_cast<float*>(w);
+  p.pdl_early = env_int("MD_KEYS_PDL_EARLY", 1);
   if (tcg) {
     p.dyn_k = 0;  // static stream-K only
+    // measured: an entry trigger lets the next kv_append pre-launch and costs ~29 us per
+    // verify -> append boundary; triggering at exit makes the appends free (tools/step_probe.py)
+    p.pdl_early = env_int("MD_TC_PDL_EARLY", 0);
     CUtensorMap qm;
     if ((st = make_qmap(&qm, q, c->batch, T, Hq, g, c->head_dim)) != MD_OK) return st;
     // the BASELINE shapes get a compile-time row count (Llama-3.1 g=4 x T=5, Qwen2.5 g=7 x T=5)

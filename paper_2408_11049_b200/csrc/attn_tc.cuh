@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                  "n"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  pdl_trigger();
+  if (p.pdl_early) pdl_trigger();
   pdl_wait();  // kv_len, the cache and q may come from the previous kernel
   fence_before();
   __syncthreads();
@@ -549,6 +549,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   fence_before();
   __syncthreads();
+  if (!p.pdl_early) pdl_trigger();
   if (warp == 5) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::TMEM_COLS));
