@@ -67,7 +67,9 @@ struct AttnParams {
   const int32_t* idx_count;   // [B] selected positions per (b, kv head)
   const int32_t* tail_start;  // [B] first position of the always-attended tail
   int idx_stride;
-  int64_t row_sB, row_sH, row_sS;  // cache strides in units of rows (d elements), for gather4
+  int64_t row_sB, row_sH, row_sS;  // cache strides in units of rows (d elements), for listed rows
+  const uint16_t* kc;              // cache K / V base pointers (listed-row copies of MODE_INDEXED)
+  const uint16_t* vc;
   unsigned long long* trace;       // diagnostics: [G][8] globaltimer stamps (md_debug_trace), or null
   int fused_merge;        // 1: the last CTA of a split unit merges (acq_rel counter); 0: attn_merge_kernel
   int* dyn;               // [2] dynamic chunk counter and finished-CTA counter (zero between calls)
@@ -329,6 +331,19 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
   constexpr int SUB = D / 64, TILE = TK * D * 2, STAGE = 2 * TILE;
   const int lane = threadIdx.x & 31;
   const bool gathered0 = (p.mode == MODE_INDEXED);
+  // MODE_INDEXED: the listed rows are copied by all 32 producer lanes with 16-byte cp.async
+  // (lane l: tile rows 2l and 2l + 1, written in the SWIZZLE_128B layout the consumers read),
+  // completing on the stage's mbarrier through cp.async.mbarrier.arrive.  (TMA tile::gather4
+  // capped this path at ~3.3 TB/s whatever the index locality; tools/gather_probe.py.)  Each
+  // lane's two row indices of the NEXT tile are loaded while the current tile is issued.
+  const int32_t* ip = gathered0 ? p.idx + ((int64_t)b * p.Hkv + kvh) * p.idx_stride : nullptr;
+  const int64_t ubase = (int64_t)b * p.row_sB + (int64_t)kvh * p.row_sH;
+  auto load_rows = [&](int pos, int nvalid, int* row) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) row[u] = (2 * lane + u < nvalid) ? __ldg(ip + pos + 2 * lane + u) : -1;
+  };
+  int rows_next[2] = {-1, -1};
+  if (gathered0 && rg.s0 < rg.e0) load_rows(rg.s0, min(TK, rg.e0 - rg.s0), rows_next);
 #pragma unroll 1
   for (int part = 0; part < 2; ++part) {
     const int rs = part ? rg.s1 : rg.s0, re = part ? rg.e1 : rg.e0;
@@ -339,28 +354,29 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
       uint8_t* kt = ring + stage * STAGE;
       uint8_t* vt = kt + TILE;
       if (part == 0 && gathered0) {
-        // rows idx[b][kvh][pos .. pos + nvalid), 4 per gather4; padding rows repeat a valid row
-        const int ngrp = (nvalid + 3) / 4;
-        if (lane == 0) {
-          mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[stage], ngrp * 4 * 128 * SUB * 2);
-        }
+        const int row[2] = {rows_next[0], rows_next[1]};
+        const int npos = pos + TK;
+        if (npos < re) load_rows(npos, min(TK, re - npos), rows_next);
+        if (lane == 0) mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
         __syncwarp();
-        if (lane < ngrp) {
-          const int32_t* ip = p.idx + ((int64_t)b * p.Hkv + kvh) * p.idx_stride + pos;
-          int row[4];
+        const uint32_t kt_a = smem_u32(kt), vt_a = smem_u32(vt);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int e = min(4 * lane + u, nvalid - 1);
-            row[u] = static_cast<int>(b * p.row_sB + kvh * p.row_sH + (int64_t)__ldg(ip + e) * p.row_sS);
-          }
-          for (int sub = 0; sub < SUB; ++sub) {
-            const int off = sub * TK * 128 + lane * 4 * 128;
-            tma_gather4(kt + off, &tm.k_rows, &full[stage], sub * 64, row[0], row[1], row[2], row[3], pol);
-            tma_gather4(vt + off, &tm.v_rows, &full[stage], sub * 64, row[0], row[1], row[2], row[3], pol);
+        for (int u = 0; u < 2; ++u) {
+          if (row[u] < 0) continue;  // rows past the tile's valid keys stay stale (masked / zeroed)
+          const int r = 2 * lane + u;
+          const int64_t off = (ubase + (int64_t)row[u] * p.row_sS) * D;
+          const uint16_t* ks = p.kc + off;
+          const uint16_t* vs = p.vc + off;
+#pragma unroll
+          for (int c = 0; c < D / 8; ++c) {
+            const uint32_t dst = (uint32_t)((c >> 3) * TK * 128 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+            cp_async16_pol(kt_a + dst, ks + c * 8, pol);
+            cp_async16_pol(vt_a + dst, vs + c * 8, pol);
           }
         }
+        cp_async_arrive(&full[stage]);  // fires when this lane's copies have landed
         __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
         continue;
       }
       if (lane != 0) continue;
@@ -1568,6 +1584,8 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.out_h0 = ix.tp ? ix.tp->rank * Hq : 0;
   p.trace = (g_trace != nullptr && g_trace_bytes >= (size_t)grid * TRACE_SLOTS * 8) ? g_trace : nullptr;
   p.fused_merge = fused_merge_enabled();
+  p.kc = static_cast<const uint16_t*>(c->k);
+  p.vc = static_cast<const uint16_t*>(c->v);
   p.row_sB = c->stride_b / c->head_dim;
   p.row_sH = c->stride_h / c->head_dim;
   p.row_sS = c->stride_s / c->head_dim;

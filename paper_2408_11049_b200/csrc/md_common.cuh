@@ -172,3 +172,16 @@ MD_DEV uint64_t globaltimer() {
   return t;
 }
 }  // namespace md
+
+namespace md {
+// 16-byte cp.async global -> shared (L2 only) with an L2 cache-policy hint
+MD_DEV void cp_async16_pol(uint32_t dst, const void* src, uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(policy)
+               : "memory");
+}
+// the mbarrier receives one arrival once every cp.async this thread issued so far has landed
+// (its pending count is raised by one now, so the phase cannot complete before that)
+MD_DEV void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+}  // namespace md

@@ -56,15 +56,19 @@ def sweep(cfg, R=3, reps=12):
 
     vms = t(lambda i: md.verify_attn_full(qv, kc[i % R], vc[i % R], kvv, mkl, scale, out_v, lse_v, ws_v))
     dms = t(lambda i: md.draft_attn_sparse(qd, kc[i % R], vc[i % R], kvd, sink, window, scale, out_d, lse_d, ws_d))
-    # SnapKV draft: 2048-token budget = 2016 listed prefix rows + the 32-token window tail
+    # SnapKV draft: 2048-token budget = 2016 listed prefix rows + the 32-token window tail,
+    # selected by md_snapkv_select from window queries of the same synthetic regime (the
+    # selection is clustered by the 5-wide pooling, as SnapKV's is)
     w_obs, budget = 32, 2048
-    rng = np.random.default_rng(0)
-    idx = np.zeros((B, Hkv, budget - w_obs), np.int32)
-    for b in range(B):
-        for h in range(Hkv):
-            idx[b, h] = np.sort(rng.choice(int(L0[b]) - w_obs, size=budget - w_obs, replace=False))
-    idx_t = torch.from_numpy(idx).cuda()
-    cnt_t = torch.full((B,), budget - w_obs, dtype=torch.int32, device="cuda")
+    q_obs = torch.empty((B, w_obs, Hq, d), dtype=torch.bfloat16, device="cuda")
+    SC.fill_q(q_obs, SEED + 7, S.T_QVERIFY, Hkv, reg)
+    plen = torch.from_numpy(L0.astype(np.int32)).cuda()
+    idx_t = torch.zeros((B, Hkv, budget), dtype=torch.int32, device="cuda")
+    cnt_t = torch.zeros(B, dtype=torch.int32, device="cuda")
+    md.snapkv_select(kc[0], vc[0], q_obs, plen, int(L0.max()), w_obs, budget, scale, idx_t, cnt_t)
+    torch.cuda.synchronize()
+    idx_np = idx_t.cpu().numpy()[:, :, : budget - w_obs]
+    runs = float(np.mean(np.diff(idx_np, axis=2) == 1))
     tail_t = torch.from_numpy((L0 - w_obs).astype(np.int32)).cuda()
     sms = t(lambda i: md.draft_attn_indexed(qd, kc[i % R], vc[i % R], kvd, idx_t, cnt_t, tail_t, scale, out_d, lse_d,
                                             ws_d))
@@ -74,6 +78,7 @@ def sweep(cfg, R=3, reps=12):
     res = {"cfg": cfg, "verify_ms": round(vms, 4), "verify_gbs": round(vb / vms / 1e6, 1),
            "draft_us": round(dms * 1e3, 2), "draft_gbs": round(db / dms / 1e6, 1),
            "snapkv_draft_us": round(sms * 1e3, 2), "snapkv_draft_gbs": round(sb / sms / 1e6, 1),
+           "snapkv_adjacent_fraction": round(runs, 3),
            "env": {k: v for k, v in os.environ.items() if k.startswith("MD_")}}
     print(json.dumps(res), flush=True)
     del kc, vc
