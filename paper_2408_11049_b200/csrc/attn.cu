@@ -957,6 +957,12 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     if ((row % C::ROWS) >= p.R) *reinterpret_cast<uint4*>(qbuf + row * C::QSTR + c * 16) = make_uint4(0, 0, 0, 0);
   }
   trace_stamp(p, 0);
+  if (warp == NC && lane == 0) {  // descriptor fetches overlap the grid-dependency wait
+    prefetch_tmap(&tm.k_full);
+    prefetch_tmap(&tm.v_full);
+    prefetch_tmap(&tm.k_part);
+    prefetch_tmap(&tm.v_part);
+  }
   if (p.pdl_early) pdl_trigger();  // else the dependent launch waits for this grid's exit
   pdl_wait();  // kv_len, the cache and q may come from the previous kernel
   trace_stamp(p, 1);

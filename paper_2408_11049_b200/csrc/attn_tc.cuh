@@ -239,6 +239,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                  "n"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  if (warp == 4 && lane == 0) {  // descriptor fetches overlap the grid-dependency wait
+    prefetch_tmap(&tm.k_full);
+    prefetch_tmap(&tm.v_full);
+    prefetch_tmap(&tm.k_part);
+    prefetch_tmap(&tm.v_part);
+    prefetch_tmap(&qmap);
+  }
   if (p.pdl_early) pdl_trigger();
   pdl_wait();  // kv_len, the cache and q may come from the previous kernel
   fence_before();
