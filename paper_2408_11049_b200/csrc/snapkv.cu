@@ -58,6 +58,28 @@ __device__ __forceinline__ void load_ktile(const Params& p, int b, int h, int k0
   }
 }
 
+// the same tile with 16-byte cp.async (rows past nkeys are left as they are: every consumer
+// masks or drops keys past the chunk); the caller commits / waits
+template <int D>
+__device__ __forceinline__ void load_ktile_async(const Params& p, int b, int h, int k0, int nkeys, uint8_t* dst) {
+  constexpr int CH = D / 8;
+  const uint32_t base = smem_u32(dst);
+  for (int i = threadIdx.x; i < KT * CH; i += THREADS) {
+    const int r = i / CH, c = i - r * CH;
+    if (r < nkeys) {
+      const void* src = reinterpret_cast<const uint4*>(p.k + b * p.sB + h * p.sH + (int64_t)(k0 + r) * p.sS) + c;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(base + (c >> 3) * (KT * 128) + swz128(r, c & 7)),
+                   "l"(src)
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_le(int n) {
+  if (n == 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+  else asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
 // Q fragments of rows mt*16 + {gq, gq+8}: row r = i*g + hh -> q[b][i][h*g + hh]
 template <int D>
 __device__ __forceinline__ void load_q(const Params& p, int b, int h, int mt, uint32_t (&qa)[D / 16][4]) {
@@ -107,7 +129,7 @@ __device__ __forceinline__ void tile_scores(const uint32_t (&qa)[D / 16][4], uin
 // pass 1: per (unit, chunk) partial (m, l) of every row over its causal keys in the chunk
 template <int D>
 __global__ void __launch_bounds__(THREADS) lse_kernel(const Params p) {
-  __shared__ __align__(1024) uint8_t ktile[KT * D * 2];
+  __shared__ __align__(1024) uint8_t ktiles[2][KT * D * 2];  // double-buffered (cp.async)
   pdl_trigger();
   pdl_wait();
   const int unit = blockIdx.x / p.nchunks, chunk = blockIdx.x - unit * p.nchunks;
@@ -124,13 +146,17 @@ __global__ void __launch_bounds__(THREADS) lse_kernel(const Params p) {
     const int lim0 = L - p.w + min(mt * 16 + gq, p.R - 1) / p.g;
     const int lim1 = L - p.w + min(mt * 16 + gq + 8, p.R - 1) / p.g;
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-    for (int k0 = k_begin; k0 < k_end; k0 += KT) {
+    __syncthreads();
+    if (k_begin < k_end) load_ktile_async<D>(p, b, h, k_begin, min(KT, k_end - k_begin), ktiles[0]);
+    int buf = 0;
+    for (int k0 = k_begin; k0 < k_end; k0 += KT, buf ^= 1) {
+      const bool more = k0 + KT < k_end;
+      if (more) load_ktile_async<D>(p, b, h, k0 + KT, min(KT, k_end - k0 - KT), ktiles[buf ^ 1]);
+      cp_async_wait_le(more ? 1 : 0);
       __syncthreads();
-      load_ktile<D>(p, b, h, k0, min(KT, k_end - k0), ktile);
-      __syncthreads();
-      if (mt >= MT) continue;
+      if (mt < MT) {
       float s[8][4];
-      tile_scores<D>(qa, smem_u32(ktile), s, p.scale_log2);
+      tile_scores<D>(qa, smem_u32(ktiles[buf]), s, p.scale_log2);
       float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -157,6 +183,8 @@ __global__ void __launch_bounds__(THREADS) lse_kernel(const Params p) {
       l1 = l1 * ex2(m1 - b1) + r1;
       m0 = n0;
       m1 = n1;
+      }
+      __syncthreads();  // every warp is done with this buffer before it is refilled
     }
     if (mt >= MT) continue;
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
@@ -175,7 +203,7 @@ __global__ void __launch_bounds__(THREADS) lse_kernel(const Params p) {
 // pass 2: lse per row from the chunk partials, then vote[j] = sum_r 2^(s_rj - lse_r), j < L - w
 template <int D>
 __global__ void __launch_bounds__(THREADS) vote_kernel(const Params p) {
-  __shared__ __align__(1024) uint8_t ktile[KT * D * 2];
+  __shared__ __align__(1024) uint8_t ktiles[2][KT * D * 2];  // double-buffered (cp.async)
   __shared__ float lse_s[256];
   __shared__ float wsum[WARPS][KT];
   pdl_trigger();
@@ -200,18 +228,33 @@ __global__ void __launch_bounds__(THREADS) vote_kernel(const Params p) {
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, cq = lane & 3;
   const int MT = (p.R + 15) / 16;
-  for (int k0 = k_begin; k0 < k_end; k0 += KT) {
+  // this warp's Q fragments stay in registers when every row tile has its own warp
+  uint32_t qown[D / 16][4];
+  const bool own = MT <= WARPS;
+  if (own && warp < MT) load_q<D>(p, b, h, warp, qown);
+  __syncthreads();  // lse_s
+  load_ktile_async<D>(p, b, h, k_begin, min(KT, k_end - k_begin), ktiles[0]);
+  int buf = 0;
+  for (int k0 = k_begin; k0 < k_end; k0 += KT, buf ^= 1) {
     float ksum[8][2];
 #pragma unroll
     for (int i = 0; i < 8; ++i) ksum[i][0] = ksum[i][1] = 0.f;
-    __syncthreads();
-    load_ktile<D>(p, b, h, k0, min(KT, k_end - k0), ktile);
+    const bool more = k0 + KT < k_end;
+    if (more) load_ktile_async<D>(p, b, h, k0 + KT, min(KT, k_end - k0 - KT), ktiles[buf ^ 1]);
+    cp_async_wait_le(more ? 1 : 0);
     __syncthreads();
     for (int mt = warp; mt < MT; mt += WARPS) {
       uint32_t qa[D / 16][4];
-      load_q<D>(p, b, h, mt, qa);
+      if (own) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) qa[kk][e] = qown[kk][e];
+      } else {
+        load_q<D>(p, b, h, mt, qa);
+      }
       float s[8][4];
-      tile_scores<D>(qa, smem_u32(ktile), s, p.scale_log2);
+      tile_scores<D>(qa, smem_u32(ktiles[buf]), s, p.scale_log2);
       const int r0 = mt * 16 + gq, r1 = r0 + 8;
       const float lse0 = r0 < p.R ? lse_s[r0] : INFINITY, lse1 = r1 < p.R ? lse_s[r1] : INFINITY;
 #pragma unroll
