@@ -91,3 +91,42 @@ def test_every_binding_declares_its_argtypes():
         if name in ("md_abi_version", "md_last_error"):
             continue
         assert getattr(lib, name).argtypes is not None, name
+
+
+def test_host_side_validation_of_selection_and_tp_calls():
+    """f1 / f4 entry points reject bad host arguments before any GPU work (no device needed)."""
+    lib = md.load_library()
+    c = _cache()
+    # tensor-parallel outputs: NULL descriptor, rank outside the world
+    st, msg = _err(lib.md_verify_attn_full_tp(ctypes.byref(c), 16, 4, 5, 16, 64, 0.1, None, None, None, 0, None))
+    assert st == md.MD_ERR_INVALID_ARG and "tp" in msg
+    bad = md.TPOut(16, 2, 2)
+    st, msg = _err(lib.md_verify_attn_full_tp(ctypes.byref(c), 16, 4, 5, 16, 64, 0.1, ctypes.byref(bad), None,
+                                              None, 0, None))
+    assert st == md.MD_ERR_INVALID_ARG and "md_tp_out" in msg
+    st, msg = _err(lib.md_draft_attn_sparse_tp(ctypes.byref(c), 16, 4, 16, 0, 0, 0.1, ctypes.byref(bad), None,
+                                               None, 0, None))
+    assert st == md.MD_ERR_INVALID_ARG
+    st, msg = _err(lib.md_tp_barrier(None, None))
+    assert st == md.MD_ERR_INVALID_ARG
+    sync = md.TPSync(16, 16, 40, 0)                       # world > 32 lanes
+    st, msg = _err(lib.md_tp_barrier(ctypes.byref(sync), None))
+    assert st == md.MD_ERR_INVALID_ARG and "world" in msg
+    st, msg = _err(lib.md_philox_u32_dev(1, None, 4, 6, 16, None))
+    assert st == md.MD_ERR_INVALID_ARG
+    # PQ selection: head_dim, GQA group, idx stride, workspace
+    st, msg = _err(lib.md_pq_select(16, 2, 8, 2, 96, 16, 16, 1024, 16, 1000, 4, 64, 100, 16, 104, 16, 16, 16,
+                                    1 << 30, None))
+    assert st == md.MD_ERR_UNSUPPORTED and "head_dim" in msg
+    st, msg = _err(lib.md_pq_select(16, 2, 64, 2, 128, 16, 16, 1024, 16, 1000, 4, 64, 100, 16, 104, 16, 16, 16,
+                                    1 << 30, None))
+    assert st == md.MD_ERR_UNSUPPORTED and "group" in msg
+    st, msg = _err(lib.md_pq_select(16, 2, 8, 2, 128, 16, 16, 1024, 16, 1000, 4, 64, 100, 16, 100, 16, 16, 16,
+                                    1 << 30, None))
+    assert st == md.MD_ERR_INVALID_ARG and "idx_stride" in msg
+    st, msg = _err(lib.md_pq_select(16, 2, 8, 2, 128, 16, 16, 1024, 16, 1000, 4, 64, 100, 16, 104, 16, 16, 16,
+                                    16, None))
+    assert st == md.MD_ERR_WORKSPACE
+    st, msg = _err(lib.md_pq_encode(ctypes.byref(_cache(d=96)), 16, 16, 10, 16, 100, None))
+    assert st == md.MD_ERR_UNSUPPORTED
+    assert md.pq_workspace_bytes(2, 2, 1000) > 0 and md.pq_workspace_bytes(0, 2, 1000) == 0
