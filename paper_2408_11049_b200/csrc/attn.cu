@@ -29,6 +29,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -1351,6 +1352,13 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // extra segment boundaries are cheap; the rows kernel (HMMA-heavy consumers that fetch Q at
 // each segment) measured slower with dynamic chunks (Llama verify 1.23 -> 1.34 ms) and its
 // static stream-K spread is small once the epilogue no longer stalls the producer.
+// tcgen05 verify kernel: dynamic chunks per CTA (MD_TC_DYN_K).  Default 0: measured slower
+// (Llama verify 1.24 -> 1.30 ms, Qwen 1.89 -> 2.08 ms with 4): every extra segment costs a Q
+// load, an O^T epilogue and a split merge, more than the per-SM bandwidth spread it removes.
+static int tc_dyn_k() {
+  static const int k = env_int("MD_TC_DYN_K", 0);
+  return k < 0 ? 0 : k;
+}
 static int dyn_k_for(int R) {
   static const int k = env_int("MD_DYN_K", 4);
   static const int rows = env_int("MD_DYN_ROWS", 0);  // 1: also the rows kernel (tests, experiments)
@@ -1373,7 +1381,9 @@ constexpr int MAX_UNITS = 65536;  // B * Hkv
 constexpr size_t COUNTER_BYTES = ((size_t)(MAX_UNITS + 2) * 4 + 255) & ~size_t(255);
 static size_t workspace_for(int G, int units, int R, int D) {
   (void)units;
-  const size_t C = (size_t)G * (1 + dyn_k_for(R));
+  // partial slots for the mma.sync kernels' grid, or the tcgen05 kernel's (1 CTA / SM, dynamic
+  // chunks), whichever is larger (the workspace query does not know which kernel will run)
+  const size_t C = std::max((size_t)G * (1 + dyn_k_for(R)), (size_t)device_sm_count() * (1 + tc_dyn_k()));
   const size_t X = use_keys_kernel(R) ? 0 : (size_t)G * XS_FRAGS * 16 * D * 4;  // rows-kernel scratch
   return COUNTER_BYTES + align256(C * 2 * R * D * 4) + align256(C * 2 * R * 4) + align256(X);
 }
@@ -1595,7 +1605,7 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.row_sB = c->stride_b / c->head_dim;
   p.row_sH = c->stride_h / c->head_dim;
   p.row_sS = c->stride_s / c->head_dim;
-  p.dyn_k = dyn_k_for(R);
+  p.dyn_k = tcg ? tc_dyn_k() : dyn_k_for(R);  // the tcgen05 kernel's dynamic tail (make_plan)
   p.dyn_static_permille = dyn_static_permille();
   p.dyn_min_tiles = dyn_min_tiles();
   const size_t chunks = (size_t)grid * (1 + p.dyn_k);
@@ -1610,7 +1620,6 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.ws_x = use_keys_kernel(R) ? nullptr : reinterpret_cast<float*>(w);
   p.pdl_early = env_int("MD_KEYS_PDL_EARLY", 1);
   if (tcg) {
-    p.dyn_k = 0;  // static stream-K only
     // measured: an entry trigger lets the next kv_append pre-launch and costs ~29 us per
     // verify -> append boundary; triggering at exit makes the appends free (tools/step_probe.py)
     p.pdl_early = env_int("MD_TC_PDL_EARLY", 0);

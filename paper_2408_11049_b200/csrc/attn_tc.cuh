@@ -202,7 +202,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* pempty = pfull + 1;      // [1]
   uint64_t* ofull = pempty + 1;      // [2]
   uint64_t* oempty = ofull + 2;      // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(oempty + 2);
+  uint64_t* cfull = oempty + 2;      // [2] dynamic chunk hand-off, producer -> MMA + softmax
+  uint64_t* cempty = cfull + 2;      // [2]
+  int* cids = reinterpret_cast<int*>(cempty + 2);  // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(cids + 2);
   int* flag = reinterpret_cast<int*>(tslot + 4);                 // [16] finish_unit
   Plan* plan_smem = reinterpret_cast<Plan*>(flag + 16);          // 40 bytes (reserved 64)
   float* red = reinterpret_cast<float*>(flag + 32);              // [4][NP] per-warp row maxima / sums
@@ -226,6 +229,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     mbar_init(pfull, 4);
     mbar_init(pempty, 1);
+    for (int s2 = 0; s2 < 2; ++s2) {
+      mbar_init(&cfull[s2], 1);
+      mbar_init(&cempty[s2], 5);  // the MMA thread + one arrival per softmax warp
+    }
     fence_mbar_init();
   }
   // Q rows >= R stay zero for the whole kernel (the TMA boxes write rows < R only)
@@ -256,7 +263,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0) *plan_smem = make_plan(p, total_tiles(p, pre), gridDim.x);
   __syncthreads();
   const Plan& pl = *plan_smem;
-  const int chunk = blockIdx.x;
+  int chunk = blockIdx.x;  // this CTA's static chunk, then the dynamic ones its producer claims
   const bool active = (int)blockIdx.x < pl.G;
   SegWalker walk;
   Seg sg;
@@ -271,11 +278,31 @@ __global__ void __launch_bounds__(THREADS, 1)
       prefetch_tmap(&tm.v_part);
       prefetch_tmap(&qmap);
       const uint64_t pol = policy_evict_first();
-      int it = 0, qi = 0;
+      int it = 0, qi = 0, ck = 0;
       long long tw = 0;
       long long* twp = p.trace ? &tw : nullptr;
-      while (walk.next(p, pre, sg))
+      // dynamic tail (long calls, see make_plan): chunks claimed one ahead from an atomic
+      // counter and handed to the MMA and softmax roles through a 2-slot mbarrier ring
+      int ahead = 0;
+      if (pl.nch > pl.G) ahead = atomicAdd(p.dyn, 1);
+      while (true) {
+        if (!walk.next(p, pre, sg)) {
+          if (pl.nch == pl.G) break;
+          const int c = pl.G + ahead;
+          const int nxt = c < pl.nch ? c : -1;
+          if (nxt >= 0) ahead = atomicAdd(p.dyn, 1);
+          const int cs = ck & 1;
+          mbar_wait(&cempty[cs], ((ck >> 1) & 1) ^ 1);
+          cids[cs] = nxt;
+          mbar_arrive(&cfull[cs]);
+          ++ck;
+          if (nxt < 0) break;
+          chunk = nxt;
+          walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+          continue;
+        }
         produce<NP>(p, tm, &qmap, sg, seg_ranges(p, sg), ring, qbuf, full, empty, qfull, qempty, it, qi, pol, twp);
+      }
       if (p.trace) trace_put(p, 15, tw);
     }
   } else if (warp == 5) {
@@ -304,7 +331,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (pv_last) commit(&ofull[pv_ob]);
         pv_stage = -1;
       };
-      while (walk.next(p, pre, sg)) {
+      int ck = 0;
+      auto next_seg = [&]() -> bool {  // mirrors the producer's chunk sequence
+        while (!walk.next(p, pre, sg)) {
+          if (pl.nch == pl.G) return false;
+          const int cs = ck & 1;
+          mbar_wait(&cfull[cs], (ck >> 1) & 1);
+          const int nxt = cids[cs];
+          mbar_arrive(&cempty[cs]);
+          ++ck;
+          if (nxt < 0) return false;
+          chunk = nxt;
+          walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+        }
+        return true;
+      };
+      while (next_seg()) {
         const Ranges rg = seg_ranges(p, sg);
         const int ns = seg_stages(rg);
         const int qs = qi % NQ, ob = si & 1;
@@ -362,7 +404,23 @@ __global__ void __launch_bounds__(THREADS, 1)
     tsec = tn;                               \
   }
     float mr[NP], lacc[NP];
-    while (walk.next(p, pre, sg)) {
+    int ck = 0;
+    auto next_seg = [&]() -> bool {  // mirrors the producer's chunk sequence
+      while (!walk.next(p, pre, sg)) {
+        if (pl.nch == pl.G) return false;
+        const int cs = ck & 1;
+        mbar_wait(&cfull[cs], (ck >> 1) & 1);
+        const int nxt = cids[cs];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty[cs]);
+        ++ck;
+        if (nxt < 0) return false;
+        chunk = nxt;
+        walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+      }
+      return true;
+    };
+    while (next_seg()) {
       const int b = sg.b, kvh = sg.kvh, n = sg.n;
       const Ranges rg = seg_ranges(p, sg);
       const int ns = seg_stages(rg);
@@ -553,6 +611,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int k = 0; k < 6; ++k) trace_put(p, k, sec[k]);
     }
 #undef TSEC
+  }
+  // the last CTA to finish re-arms the dynamic counters for the next call (every producer has
+  // made its final claim before any role saw the -1 hand-off)
+  if (active && pl.nch > pl.G && threadIdx.x == 0) {
+    if (atomicAdd(p.dyn + 1, 1) == pl.G - 1) {
+      p.dyn[0] = 0;
+      p.dyn[1] = 0;
+    }
   }
   fence_before();
   __syncthreads();
