@@ -36,6 +36,7 @@
 
 #include "md_common.cuh"
 #include "md_internal.h"
+#include "tcgen05.cuh"
 
 namespace md {
 
