@@ -17,8 +17,14 @@
 
 #include <cmath>
 
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <mutex>
+
 #include "md_common.cuh"
 #include "md_internal.h"
+#include "tcgen05.cuh"
 
 namespace md {
 namespace snap {
@@ -386,12 +392,330 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const Params p) {
 
 }  // namespace snap
 
+// ============================================================================ tcgen05 passes
+// S1/S2 on the 5th-generation tensor cores (head_dim 128, R = g*w <= 256 window-query rows):
+// S[rows][128 keys] = Q . K^T with the rows on the MMA M dimension (one or two 128-row tiles)
+// and the accumulator in TMEM, so thread x of softmax warp group m owns row m*128 + x and the
+// lse pass is thread-local (online max / sum over its row); the vote pass turns its row into
+// 2^(s - lse_r) and sums the 128 rows of every key column with a warp butterfly reduce-scatter
+// (31 shuffles per 32 columns) plus a shared-memory sum over the warps.  Q arrives by one TMA
+// box per 64-column slab (rows r = i*g + h in order), K by the 64-/16-row boxes of the verify
+// kernel into a 3-stage ring; one thread issues the MMAs (K-major SWIZZLE_128B operands).
+namespace snaptc {
+
+constexpr int KT = 128;            // keys per stage (MMA N)
+constexpr int SLAB = KT * 128;     // one 64-column slab of a 128-key K tile
+constexpr int KSTAGE = 2 * SLAB;   // K only (32 KB)
+constexpr int CHUNK = 4096;        // keys per CTA (32 stages: the CTA setup is amortised)
+constexpr int BOXF = 64, BOXP = 16;  // full / partial TMA box rows
+
+template <int NM>
+struct Cfg {
+  static constexpr int NSTAGE = NM == 1 ? 2 : 3;  // NM = 1: 2 CTAs / SM
+  static constexpr int QROWS = NM * 128;
+  static constexpr int QBUF = 2 * QROWS * 128;
+  static constexpr int NSW = NM * 4;                     // softmax warps
+  static constexpr int THREADS = NSW * 32 + 64;          // + producer warp + MMA warp
+  static constexpr int AUX = NSW * KT * 4 + QROWS * 4 + 512;
+  static constexpr int SMEM = NSTAGE * KSTAGE + QBUF + AUX + 1024;
+  static constexpr int CTAS = NM == 1 ? 2 : 1;
+  static constexpr int TMEM_COLS = 2 * NM * KT <= 256 ? 256 : 512;
+};
+
+template <int PASS, int NM>
+__global__ void __launch_bounds__(Cfg<NM>::THREADS, Cfg<NM>::CTAS)
+    snap_tc_kernel(const __grid_constant__ CUtensorMap kfull, const __grid_constant__ CUtensorMap kpart,
+                   const __grid_constant__ CUtensorMap qmap, const snap::Params p) {
+  using C = Cfg<NM>;
+  constexpr int NSTAGE = C::NSTAGE;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ring = smem;
+  uint8_t* qbuf = ring + NSTAGE * KSTAGE;
+  float* wsum = reinterpret_cast<float*>(qbuf + C::QBUF);  // [NSW][KT] vote partial sums
+  float* lse_s = wsum + C::NSW * KT;                       // [QROWS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(lse_s + C::QROWS);
+  uint64_t* empty = full + NSTAGE;
+  uint64_t* qfull = empty + NSTAGE;
+  uint64_t* sfull = qfull + 1;   // [2]
+  uint64_t* sempty = sfull + 2;  // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int unit = blockIdx.x / p.nchunks, chunk = blockIdx.x - unit * p.nchunks;
+  const int b = unit / p.Hkv, h = unit - b * p.Hkv;
+  pdl_wait();  // q_obs / the cache (and, for the vote pass, the lse partials) are ready
+  const int L = __ldg(p.L + b);
+  const int k_begin = chunk * CHUNK;
+  const int k_end = PASS == 0 ? min(L, k_begin + CHUNK) : min(L - p.w, k_begin + CHUNK);
+  if (k_begin >= k_end) {  // uniform: a chunk past the prompt (lse pass: an empty partial)
+    if (PASS == 0)
+      for (int r = threadIdx.x; r < p.R; r += blockDim.x) {
+        float* base = p.part + ((int64_t)unit * p.nchunks + chunk) * p.R * 2;
+        base[r * 2] = -INFINITY;
+        base[r * 2 + 1] = 0.f;
+      }
+    pdl_trigger();
+    return;
+  }
+  if (threadIdx.x == 0) {
+    for (int s2 = 0; s2 < NSTAGE; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], 1);
+    }
+    mbar_init(qfull, 1);
+    for (int s2 = 0; s2 < 2; ++s2) {
+      mbar_init(&sfull[s2], 1);
+      mbar_init(&sempty[s2], C::NSW);
+    }
+    fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < C::QBUF / 16; i += blockDim.x) {  // Q rows >= R stay zero
+    if (((i * 16) / 128) % C::QROWS >= p.R) reinterpret_cast<uint4*>(qbuf)[i] = make_uint4(0, 0, 0, 0);
+  }
+  fence_proxy_async();
+  if (warp == C::NSW + 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = *tslot;
+  const int nst = (k_end - k_begin + KT - 1) / KT;
+
+  if (warp == C::NSW) {
+    // ============================== TMA producer ==============================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      mbar_arrive_expect_tx(qfull, 2 * p.R * 128);
+      for (int sub = 0; sub < 2; ++sub) tma_load_4d(qbuf + sub * C::QROWS * 128, &qmap, qfull, sub * 64, h * p.g, 0, b, pol);
+      for (int j = 0; j < nst; ++j) {
+        const int stage = j % NSTAGE, pos = k_begin + j * KT, nvalid = min(KT, k_end - pos);
+        uint8_t* kt = ring + stage * KSTAGE;
+        mbar_wait(&empty[stage], ((j / NSTAGE) & 1) ^ 1);
+        int bytes = 0;
+        for (int hf = 0; hf < 2; ++hf) {
+          const int hv = nvalid - hf * BOXF;
+          if (hv >= BOXF) bytes += 2 * BOXF * 128;
+          else if (hv > 0) bytes += 2 * ((hv + BOXP - 1) / BOXP) * BOXP * 128;
+        }
+        mbar_arrive_expect_tx(&full[stage], bytes);
+        for (int hf = 0; hf < 2; ++hf) {
+          const int hv = nvalid - hf * BOXF, r0 = pos + hf * BOXF;
+          for (int sub = 0; sub < 2; ++sub) {
+            const int off = sub * SLAB + hf * BOXF * 128;
+            if (hv >= BOXF) {
+              tma_load_4d(kt + off, &kfull, &full[stage], sub * 64, r0, h, b, pol);
+            } else if (hv > 0) {
+              for (int bx = 0; bx * BOXP < hv; ++bx)
+                tma_load_4d(kt + off + bx * BOXP * 128, &kpart, &full[stage], sub * 64, r0 + bx * BOXP, h, b, pol);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == C::NSW + 1) {
+    // ============================== MMA issuer ==============================
+    if (lane == 0) {
+      constexpr uint32_t ID = tc::idesc(128, KT, 0, 0);
+      const uint32_t ring_a = smem_u32(ring), q_a = smem_u32(qbuf);
+      mbar_wait(qfull, 0);
+      for (int j = 0; j < nst; ++j) {
+        const int stage = j % NSTAGE, sb = j & 1;
+        mbar_wait(&full[stage], (j / NSTAGE) & 1);
+        mbar_wait(&sempty[sb], ((j >> 1) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t kt = ring_a + stage * KSTAGE;
+#pragma unroll
+        for (int m = 0; m < NM; ++m)
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * SLAB + (kk & 3) * 32;
+            const uint32_t qoff = (kk >> 2) * (C::QROWS * 128) + m * 128 * 128 + (kk & 3) * 32;
+            tc::mma_f16(tbase + (sb * NM + m) * KT, tc::sdesc(q_a + qoff, 16, 1024, 2), tc::sdesc(kt + off, 16, 1024, 2),
+                        ID, kk > 0 ? 1u : 0u);
+          }
+        tc::commit(&sfull[sb]);
+        tc::commit(&empty[stage]);
+      }
+    }
+  } else {
+    // ============================== row threads ==============================
+    const int m = warp >> 2, x = threadIdx.x;           // row r = x (warps 0..NSW-1)
+    const int r = x;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const bool live = r < p.R;
+    const int lim = live ? L - p.w + r / p.g : -1;       // causal limit of window query i = r / g
+    float mrow = -INFINITY, lrow = 0.f, lse = INFINITY;
+    if (PASS == 1 && live) {  // lse_r from the chunk partials of the lse pass
+      const int nch = (L + CHUNK - 1) / CHUNK;
+      const float* base = p.part + (int64_t)unit * p.nchunks * p.R * 2 + r * 2;
+      float M = -INFINITY;
+      for (int c2 = 0; c2 < nch; ++c2) M = fmaxf(M, base[(int64_t)c2 * p.R * 2]);
+      float S = 0.f;
+      for (int c2 = 0; c2 < nch; ++c2) {
+        const float l = base[(int64_t)c2 * p.R * 2 + 1];
+        if (l > 0.f) S += l * ex2(base[(int64_t)c2 * p.R * 2] - M);
+      }
+      lse = M + __log2f(S);
+    }
+    const float sl2 = p.scale_log2;
+    for (int j = 0; j < nst; ++j) {
+      const int sb = j & 1, pos = k_begin + j * KT;
+      mbar_wait(&sfull[sb], (j >> 1) & 1);
+      tc::fence_after();
+      const uint32_t ta = tbase + (sb * NM + m) * KT + lane_off;
+#pragma unroll 1
+      for (int c = 0; c < KT; c += 32) {
+        float v[32];
+        tc::tld16(ta + c, v);
+        tc::tld16(ta + c + 16, v + 16);
+        tc::wait_ld();
+        if (PASS == 0) {
+          float mx = -INFINITY;
+          if (pos + c + 32 <= k_end && pos + c + 31 <= L - p.w && live) {  // no key masked
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+              v[t] *= sl2;
+              mx = fmaxf(mx, v[t]);
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+              const int key = pos + c + t;
+              v[t] = (live && key < k_end && key <= lim) ? v[t] * sl2 : -INFINITY;
+              mx = fmaxf(mx, v[t]);
+            }
+          }
+          const float mn = fmaxf(mrow, mx);
+          const float base = (mn == -INFINITY) ? 0.f : mn;
+          float sum = 0.f;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) sum += ex2(v[t] - base);
+          lrow = lrow * ex2(mrow - base) + sum;
+          mrow = mn;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int key = pos + c + t;
+            v[t] = (live && key < k_end) ? ex2(v[t] * sl2 - lse) : 0.f;
+          }
+          // butterfly reduce-scatter over the warp: lane t ends with column t's sum of 32 rows
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) {
+            const bool hi = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < o; ++i) {
+              const float keep = hi ? v[i + o] : v[i];
+              const float send = hi ? v[i] : v[i + o];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+          }
+          wsum[warp * KT + c + lane] = v[0];
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[sb]);
+      if (PASS == 1) {
+        named_bar_sync(2, C::NSW * 32);
+        if (x < KT && pos + x < k_end) {
+          float vsum = 0.f;
+#pragma unroll
+          for (int w2 = 0; w2 < C::NSW; ++w2) vsum += wsum[w2 * KT + x];
+          p.vote[(int64_t)unit * p.maxL + pos + x] = vsum;
+        }
+        named_bar_sync(2, C::NSW * 32);  // wsum is rewritten by the next stage
+      }
+    }
+    if (PASS == 0 && live) {
+      float* base = p.part + ((int64_t)unit * p.nchunks + chunk) * p.R * 2;
+      base[r * 2] = mrow;
+      base[r * 2 + 1] = lrow;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  pdl_trigger();
+  if (warp == C::NSW + 1) {
+    tc::fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::TMEM_COLS));
+  }
+}
+
+}  // namespace snaptc
+
 static size_t snap_align(size_t x) { return (x + 255) & ~size_t(255); }
 
 static size_t snap_ws(int B, int Hkv, int R, int maxL) {
   const int nchunks = (maxL + snap::CHUNK - 1) / snap::CHUNK;
   const size_t units = (size_t)B * Hkv;
   return snap_align(units * nchunks * R * 2 * 4) + 2 * snap_align(units * maxL * 4);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 snap_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+static bool snap_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                     const cuuint32_t* box) {
+  auto enc = snap_encode();
+  if (enc == nullptr) return false;
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NM>
+static md_status snap_tc_launch(const md_kv_cache* c, const void* q_obs, const snap::Params& p, unsigned grid,
+                                cudaStream_t s) {
+  using C = snaptc::Cfg<NM>;
+  CUtensorMap kf, kp, qm;
+  const cuuint64_t kd[4] = {(cuuint64_t)c->head_dim, (cuuint64_t)c->capacity, (cuuint64_t)c->num_kv_heads,
+                            (cuuint64_t)c->batch};
+  const cuuint64_t ks[3] = {(cuuint64_t)c->stride_s * 2, (cuuint64_t)c->stride_h * 2, (cuuint64_t)c->stride_b * 2};
+  const cuuint32_t kbf[4] = {64, (cuuint32_t)snaptc::BOXF, 1, 1}, kbp[4] = {64, (cuuint32_t)snaptc::BOXP, 1, 1};
+  const cuuint64_t qd[4] = {(cuuint64_t)c->head_dim, (cuuint64_t)p.Hq, (cuuint64_t)p.w, (cuuint64_t)p.B};
+  const cuuint64_t qs[3] = {(cuuint64_t)c->head_dim * 2, (cuuint64_t)p.Hq * c->head_dim * 2,
+                            (cuuint64_t)p.w * p.Hq * c->head_dim * 2};
+  const cuuint32_t qb[4] = {64, (cuuint32_t)p.g, (cuuint32_t)p.w, 1};
+  MD_REQUIRE(snap_map(&kf, c->k, 4, kd, ks, kbf) && snap_map(&kp, c->k, 4, kd, ks, kbp) &&
+                 snap_map(&qm, q_obs, 4, qd, qs, qb),
+             MD_ERR_INVALID_ARG, "md_snapkv_select: cuTensorMapEncodeTiled failed (strides / alignment)");
+  static int done_dev = -1;  // per-process; the attribute call is idempotent (benign race)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done_dev != dev) {
+    if (cudaFuncSetAttribute(snaptc::snap_tc_kernel<0, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(snaptc::snap_tc_kernel<1, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) !=
+            cudaSuccess)
+      return check_launch("cudaFuncSetAttribute");
+    done_dev = dev;
+  }
+  launch_pdl(snaptc::snap_tc_kernel<0, NM>, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, s, kf, kp, qm, p);
+  launch_pdl(snaptc::snap_tc_kernel<1, NM>, dim3(grid), dim3(C::THREADS), (size_t)C::SMEM, s, kf, kp, qm, p);
+  return check_launch("snap_tc_kernel");
+}
+
+static bool snap_tc_enabled() {  // MD_SNAP_TC=0: the mma.sync passes
+  static const bool v = [] {
+    const char* e = getenv("MD_SNAP_TC");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
 }
 
 }  // namespace md
@@ -455,7 +779,13 @@ extern "C" MD_API md_status md_snapkv_select(const md_kv_cache* c, const void* q
   p.keep = budget - w;
   cudaStream_t s = (cudaStream_t)stream;
   const unsigned grid = static_cast<unsigned>(units * p.nchunks);
-  if (c->head_dim == 128) {
+  if (c->head_dim == 128 && snap_tc_enabled()) {
+    p.nchunks = (max_prefill_len + snaptc::CHUNK - 1) / snaptc::CHUNK;  // <= the workspace's chunk count
+    const unsigned grid_tc = static_cast<unsigned>(units * p.nchunks);
+    const md_status st = (p.R <= 128) ? snap_tc_launch<1>(c, q_obs, p, grid_tc, s)
+                                   : snap_tc_launch<2>(c, q_obs, p, grid_tc, s);
+    if (st != MD_OK) return st;
+  } else if (c->head_dim == 128) {
     launch_pdl(snap::lse_kernel<128>, dim3(grid), dim3(snap::THREADS), 0, s, p);
     launch_pdl(snap::vote_kernel<128>, dim3(grid), dim3(snap::THREADS), 0, s, p);
   } else {

@@ -112,6 +112,7 @@ def _check_selection(idx_gpu, cnt_gpu, idx_ref, cnt_ref, pooled_ref, rel_tol=1e-
     (3, 32, 8, 128, [1500, 1400, 700], 32, 512, "flat"),
     (2, 28, 4, 128, [2500, 300], 32, 1024, "peaky"),          # short prompt: keep everything
     (2, 4, 4, 64, [900, 1000], 8, 100, "peaky"),
+    (1, 32, 8, 128, [9100], 32, 512, "peaky"),                 # several 4096-key tcgen05 chunks
 ])
 def test_snapkv_select_matches_oracle(B, Hq, Hkv, d, L, w, budget, regime):
     import synth as S
@@ -127,3 +128,16 @@ def test_snapkv_select_matches_oracle(B, Hq, Hkv, d, L, w, budget, regime):
     torch.cuda.synchronize()
     ref_idx, ref_cnt, pooled = SK.snapkv_select(q_obs_bits, case.k_bits, np.array(L), w, budget, case.scale)
     _check_selection(idx.cpu().numpy(), cnt.cpu().numpy(), ref_idx, ref_cnt, pooled)
+
+
+def test_snapkv_select_mma_sync_path():
+    """The mma.sync passes (MD_SNAP_TC=0; also every head_dim-64 call) on the d=128 cases."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MD_SNAP_TC="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_snapkv.py"), "-k", "matches_oracle"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
