@@ -375,13 +375,14 @@ def run_gpu(args):
                layers * (h_qv.nbytes + h_kv.nbytes + h_vv.nbytes) + h_p.nbytes + h_q.nbytes + h_d.nbytes)
         d2h = h_out.nbytes + h_n.nbytes
 
-        # Copies run on their own streams, double-buffered per call, so the H2D traffic of
-        # call c+2 overlaps the kernels of call c (a serving loop would prefetch the same way).
+        # Copies run on their own stream into NB staging slots per call kind, so the H2D traffic
+        # of call c+NB-1 overlaps the kernels of call c (a serving loop would prefetch the same way).
         copy_s = torch.cuda.Stream()
-        st_d = [(torch.empty_like(qd), torch.empty_like(knew_d), torch.empty_like(vnew_d)) for _ in range(2)]
-        st_v = [(torch.empty_like(qv), torch.empty_like(knew_v), torch.empty_like(vnew_v)) for _ in range(2)]
-        ready = [torch.cuda.Event() for _ in range(2)]
-        done = [torch.cuda.Event() for _ in range(2)]
+        NB = 4  # staging slots: a call's inputs are copied NB - 1 calls ahead of it
+        st_d = [(torch.empty_like(qd), torch.empty_like(knew_d), torch.empty_like(vnew_d)) for _ in range(NB)]
+        st_v = [(torch.empty_like(qv), torch.empty_like(knew_v), torch.empty_like(vnew_v)) for _ in range(NB)]
+        ready = [torch.cuda.Event() for _ in range(NB)]
+        done = [torch.cuda.Event() for _ in range(NB)]
         pq_ready, acc_done = torch.cuda.Event(), torch.cuda.Event()
         ncalls = gamma * layers + layers
 
@@ -391,7 +392,7 @@ def run_gpu(args):
         bounds = [[(n * c) // ncalls for c in range(ncalls + 1)] for n in (x[0].numel() for x in flat_pq)]
 
         def issue_copy(c):
-            sl = c % 2
+            sl = c % NB
             with torch.cuda.stream(copy_s):
                 copy_s.wait_event(done[sl])
                 dst, src = (st_d[sl], (h_qd, h_kd, h_vd)) if c < gamma * layers else (st_v[sl], (h_qv, h_kv, h_vv))
@@ -408,11 +409,11 @@ def run_gpu(args):
 
         def e2e_step(i):
             cur = torch.cuda.current_stream()
-            issue_copy(0)
-            issue_copy(1)
+            for c0 in range(min(NB - 1, ncalls)):
+                issue_copy(c0)
             torch.add(committed[None, :], ar, out=pos_buf)
             for c in range(ncalls):
-                sl = c % 2
+                sl = c % NB
                 cur.wait_event(ready[sl])
                 l = c % layers
                 kb, vb_ = kc[l % R], vc[l % R]
@@ -430,8 +431,8 @@ def run_gpu(args):
                     if world > 1:
                         gather_rank_major(out_v, gath_v)
                 done[sl].record(cur)
-                if c + 2 < ncalls:
-                    issue_copy(c + 2)
+                if c + NB - 1 < ncalls:
+                    issue_copy(c + NB - 1)
             cur.wait_event(pq_ready)
             md.philox_u32(SEED, i, rnd)
             md.spec_accept(p_t, q_t, dtok, rnd, out_tok, nacc, committed, mode="sample")
