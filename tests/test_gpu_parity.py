@@ -65,6 +65,9 @@ VERIFY_CASES = [
     ("decode_T1",      2, 32, 8, 128, 1, [300, 1]),
     ("gqa_g8_T8",      2, 16, 2, 64, 8, [130, 8]),       # 64 rows = 4 m-tiles
     ("d64_ragged",     4, 8, 2, 64, 3, [3, 65, 128, 129]),
+    ("tc_generic_24",  2, 16, 4, 128, 6, [2000, 133]),       # tcgen05 kernel, NP=32, runtime R=24
+    ("tc_generic_40",  2, 16, 2, 128, 5, [1500, 700]),       # tcgen05 kernel, NP=48, runtime R=40
+    ("tc_np16_16",     2, 8, 2, 128, 4, [900, 260]),         # tcgen05 kernel, NP=16, R=16
 ]
 
 
