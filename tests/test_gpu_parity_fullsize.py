@@ -20,6 +20,8 @@ FULL = [
     ("llama2_8k", 64, 32, 32, 128, 8192, 3, 4, 508),
     ("llama3_b64_32k", 64, 32, 8, 128, 32768, 4, 4, 1020),
     ("qwen_100k", 64, 28, 4, 128, 100000, 4, 4, 2044),
+    ("llama3_32k", 128, 32, 8, 128, 32768, 4, 4, 1020),
+    ("llama3_scaling", 256, 32, 8, 128, 32768, 4, 4, 1020),
 ]
 
 
