@@ -1543,12 +1543,13 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
     MD_REQUIRE(ix.tp->out_peers != nullptr && ix.tp->world >= 1 && ix.tp->rank >= 0 && ix.tp->rank < ix.tp->world &&
                    ix.tp->world <= 64,
                MD_ERR_INVALID_ARG, "%s: bad md_tp_out (need out_peers, 0 <= rank < world <= 64)", who);
-    out = reinterpret_cast<float*>(16);  // unused: every output row goes to out_peers
   }
-  MD_REQUIRE(q != nullptr && kv_len != nullptr && out != nullptr, MD_ERR_INVALID_ARG, "%s: NULL q/kv_len/out", who);
+  MD_REQUIRE(q != nullptr && kv_len != nullptr && (out != nullptr || ix.tp != nullptr), MD_ERR_INVALID_ARG,
+             "%s: NULL q/kv_len/out", who);
   MD_REQUIRE(Hq >= 1 && Hq % c->num_kv_heads == 0, MD_ERR_INVALID_ARG, "%s: num_q_heads must be a multiple of Hkv",
              who);
   MD_REQUIRE(aligned16(q) && aligned16(out), MD_ERR_INVALID_ARG, "%s: q and out must be 16-byte aligned", who);
+  // (with tensor-parallel outputs `out` is NULL: every output row goes to ix.tp->out_peers)
   const int g = Hq / c->num_kv_heads;
   const int R = g * T;
   MD_REQUIRE(R <= 64, MD_ERR_UNSUPPORTED, "%s: g*T = %d > 64 query rows per KV head is not supported", who, R);

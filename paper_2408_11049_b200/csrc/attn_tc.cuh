@@ -562,6 +562,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       trace_put(p, 12, w_sf);
       trace_put(p, 13, w_pe);
       trace_put(p, 14, clock64() - t_start);
+      trace_put(p, 6, globaltimer());  // softmax end (ns): the CTA's finish time
       for (int k = 0; k < 6; ++k) trace_put(p, k, sec[k]);
     }
 #undef TSEC

@@ -49,4 +49,6 @@ res = {"cfg": cfg, "ctas": int(len(t)), "call_us": round(a.elapsed_time(b) * 1e3
        "tiles_per_cta": float(np.median(t[:, 11]))}
 for i, nme in names.items():
     res[nme + "_kcyc_p50"] = round(float(np.median(t[:, i])) / 1e3, 1)
+ends = t[:, 6]
+res["finish_spread_us"] = [round(float(x), 1) for x in np.percentile((ends - ends.min()) / 1e3, [0, 10, 50, 90, 100])]
 print(json.dumps(res))
