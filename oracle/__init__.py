@@ -21,6 +21,9 @@ Modules
   philox     O5         : Philox4x32-10 counter-based uniforms
   theory     Eq.1       : expected generation length and accepted-count PMF
   enumerate  O4 pins    : exact rational output distribution on tiny vocabularies
+  snapkv     f2         : SnapKV selection (votes, pooling, top-k) and index-list draft attention
+  tree       f3         : tree-masked verify, tree acceptance, KV compaction
+  pqcache    f4         : PQ encode, fixed-point lookup-table scores, exact top-k selection
 
 Parity pins: every function is pinned in tests/test_oracle_*.py; see DESIGN.md
 §4 for the list.  No function here is "parity unpinned".
