@@ -203,12 +203,33 @@ def run_gpu(args):
                        dtype=torch.uint8, device=dev)
     gath_v = torch.empty((world, B, T, Hq, d), device=dev) if world > 1 else None
     gath_d = torch.empty((world, B, Hq, d), device=dev) if world > 1 else None
-    # f1: --tp-exchange p2p replaces the all-gather with peer stores + md_tp_barrier
+    # f1: the fused exchange (peer stores + md_tp_barrier) replaces the all-gather when the peer
+    # buffers can be mapped and a self-test call agrees bit for bit with the NCCL all-gather of
+    # the plain call; otherwise (or with --tp-exchange nccl) the NCCL all-gather is used
     xv = xd = None
-    if world > 1 and args.tp_exchange == "p2p":
-        from paper_2408_11049_b200.tp import PeerExchange
-        xv = PeerExchange((B, T, Hq_full, d))
-        xd = PeerExchange((B, Hq_full, d))
+    exchange = "nccl" if world > 1 else "none"
+    if world > 1 and args.tp_exchange in ("p2p", "auto"):
+        ok = 1
+        try:
+            from paper_2408_11049_b200.tp import PeerExchange, gather_heads
+            xv = PeerExchange((B, T, Hq_full, d))
+            xd = PeerExchange((B, Hq_full, d))
+            kv_t = torch.from_numpy((L0 + 1).astype(np.int32)).to(dev)
+            md.draft_attn_sparse_tp(qd, kc[0], vc[0], kv_t, sink, window, scale, xd.out, None, ws_d)
+            xd.barrier()
+            md.draft_attn_sparse(qd, kc[0], vc[0], kv_t, sink, window, scale, out_d, None, ws_d)
+            ref = gather_heads(out_d, world)
+            torch.cuda.synchronize()
+            ok = int(torch.equal(xd.buf, ref))
+        except Exception as e:  # noqa: BLE001 - any failure selects the NCCL path
+            print(f"rank {rank}: fused exchange unavailable ({type(e).__name__}: {e}); using NCCL", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            exchange = "p2p"
+        else:
+            xv = xd = None
 
     def layer_pass(pos):
         # pos[j] = committed + j  (rows: draft j start = pos[j], draft j kv_len = pos[j+1],
@@ -243,7 +264,7 @@ def run_gpu(args):
     # positions for the step are one plumbing op on the committed lengths
     pos_buf = torch.empty((gamma + 2, B), dtype=torch.int32, device=dev)
 
-    use_graph = not args.no_graph and world == 1
+    use_graph = not args.no_graph and (world == 1 or exchange == "p2p")  # NCCL calls stay eager
     graph = None
     step_dev = torch.zeros(1, dtype=torch.int64, device=dev)
 
@@ -486,7 +507,7 @@ def run_gpu(args):
                        "attention_only": True,
                        "cuda_graph": ("layer loop" if split else "whole step (drafts + verify + philox + accept)")
                        if use_graph else False,
-                       "parallelism": (f"tp{world} (KV heads, {args.tp_exchange} exchange)" if world > 1
+                       "parallelism": (f"tp{world} (KV heads, {exchange} exchange)" if world > 1
                                        else "single GPU")},
             "tokens_per_step": round(tokens / args.steps, 3),
             "gpu_launches": launches_per_step * args.steps,
@@ -611,8 +632,8 @@ def main(argv=None):
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-ar", action="store_true")
-    ap.add_argument("--tp-exchange", choices=["nccl", "p2p"], default="nccl",
-                    help="N>1: NCCL all-gather of per-head outputs, or the fused peer-store exchange (f1)")
+    ap.add_argument("--tp-exchange", choices=["auto", "nccl", "p2p"], default="auto",
+                    help="N>1: the fused peer-store exchange (f1) when it self-tests OK (auto), or NCCL")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
