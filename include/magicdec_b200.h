@@ -297,6 +297,9 @@ MD_API md_status md_pq_select(const void* q, int32_t batch, int32_t num_q_heads,
  *   lse:       local layout [B][T][Hq] (may be NULL), as the non-TP calls.
  * All other arguments and the workspace are those of md_verify_attn_full / md_draft_attn_sparse
  * with the rank-local Hq and cache.  Returns MD_ERR_INVALID_ARG for a bad md_tp_out.
+ * Every rank writes into every buffer at each call: a rank that still reads the previous
+ * call's result while a faster peer may already issue the next call should alternate two
+ * buffer sets (each with its own md_tp_sync) between consecutive calls.
  */
 typedef struct {
   float* const* out_peers;
