@@ -346,3 +346,24 @@ def test_large_batch_uses_global_walk():
     o, l = _run_draft(case, 4, 60)
     ro, rl = OA.draft_attn_sparse(case.qd_bits, case.k_bits, case.v_bits, case.kv_len, 4, 60, case.scale)
     _cmp(o, l, ro, rl)
+
+
+def test_verify_rising_scores_exercise_max_raises():
+    """Scores that climb by ~4 (log2 units) every 128 keys force the tcgen05 kernel's lazy
+    max raise (threshold 2^8) again and again inside a segment, so the thread-local row sums
+    and the O^T accumulator in TMEM are rescaled many times; also a falling sequence (the max
+    is set by the first stage and never raised)."""
+    B, Hq, Hkv, d, T = 2, 32, 8, 128, 5
+    lens = [1500, 1100]
+    case = AttnCase(B, Hq, Hkv, d, max(lens) + 8, lens, T=T, seed=97)
+    one = S.k_to_bf16_bits(np.array([32]))[0]              # 1.0
+    case.qv_bits[:] = one
+    for b in range(B):
+        for j in range(case.cap):
+            level = min(j // 128, 63) * 8                    # 0.25 * (j // 128) on the k/32 grid
+            val = S.k_to_bf16_bits(np.array([level]))[0]
+            case.k_bits[b, :, j, :] = val if b == 0 else S.k_to_bf16_bits(np.array([max(0, 96 - level)]))[0]
+    case.to_cuda()
+    o, l = _run_verify(case)
+    ro, rl = OA.verify_attn_full(case.qv_bits, case.k_bits, case.v_bits, case.kv_len, case.scale)
+    _cmp(o, l, ro, rl)
