@@ -407,10 +407,12 @@ def run_gpu(args):
         pq_ready, acc_done = torch.cuda.Event(), torch.cuda.Event()
         ncalls = gamma * layers + layers
 
-        # p / q (295 MB at the target point) are copied in ncalls slices riding along with the
-        # per-call inputs, so no call's inputs queue behind one large copy on the copy engine
+        # p / q (295 MB at the target point) are copied in slices riding along with the inputs of
+        # the verify calls (long enough to hide them), so no call's inputs queue behind one large
+        # copy and the short draft calls never wait for the copy engine
         flat_pq = [(t.view(-1), h.view(-1)) for t, h in ((p_t, h_p), (q_t, h_q))]
-        bounds = [[(n * c) // ncalls for c in range(ncalls + 1)] for n in (x[0].numel() for x in flat_pq)]
+        nd = gamma * layers                      # draft calls come first, then the verify calls
+        bounds = [[(n * c) // layers for c in range(layers + 1)] for n in (x[0].numel() for x in flat_pq)]
 
         def issue_copy(c):
             sl = c % NB
@@ -419,11 +421,13 @@ def run_gpu(args):
                 dst, src = (st_d[sl], (h_qd, h_kd, h_vd)) if c < gamma * layers else (st_v[sl], (h_qv, h_kv, h_vv))
                 for x, y in zip(dst, src):
                     x.copy_(y, non_blocking=True)
-                if c == 0:
+                if c == nd:
                     copy_s.wait_event(acc_done)  # the previous step's acceptance has read p / q
                     dtok.copy_(h_d, non_blocking=True)
-                for (t, h), bd in zip(flat_pq, bounds):
-                    t[bd[c]:bd[c + 1]].copy_(h[bd[c]:bd[c + 1]], non_blocking=True)
+                if c >= nd:
+                    v = c - nd
+                    for (t, h), bd in zip(flat_pq, bounds):
+                        t[bd[v]:bd[v + 1]].copy_(h[bd[v]:bd[v + 1]], non_blocking=True)
                 ready[sl].record(copy_s)
                 if c == ncalls - 1:
                     pq_ready.record(copy_s)
