@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) pq_encode_kernel(const uint16_t* __restri
 // ------------------------------------------------------------------ P2 + P3 lookup table
 // grid units, 256 threads: thread c computes lut[m][c] for all 16 m.
 template <int S>
-__global__ void __launch_bounds__(256) pq_lut_kernel(const uint16_t* __restrict__ q, int Hq, int Hkv,
+__global__ void __launch_bounds__(256, 4) pq_lut_kernel(const uint16_t* __restrict__ q, int Hq, int Hkv,
                                                      const uint16_t* __restrict__ cb, int32_t* __restrict__ lutq,
                                                      uint32_t* __restrict__ hist) {
   constexpr int D = S * M;
@@ -224,15 +224,22 @@ __global__ void __launch_bounds__(SCORE_THREADS, 2) pq_score_kernel(const uint8_
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int l15 = lane & 15;
-  const uint32_t tbase = smem_u32(tab) + ((lane >> 4) << 6);  // copy (lane >> 4): +16 words
-  // step i reads sub-space m = i ^ l15: its byte is byte ((i & 3) ^ rx) of word ((i >> 2) ^ qx)
-  uint32_t off[M];
+  // Step i reads sub-space m = i ^ l15 from copy (lane >> 4): byte offset within a table row
+  // ofs(i) = (lane >> 4) * 64 + (i ^ l15) * 4 < 256.  One byte permute builds the whole
+  // address: byte 0 = ofs(i) (from xo[i >> 1], which holds ofs(2p), ofs(2p + 1), 0, 0), byte
+  // 1 = the code (row c at byte c << 8), bytes 2, 3 = 0; the table base folds into the load's
+  // immediate offset (tab is a shared-memory symbol), so a lookup is PRMT + LDS.
+  const uint32_t cpo = (uint32_t)((lane >> 4) << 6);
+  uint32_t xo[M / 2];
 #pragma unroll
-  for (int i = 0; i < M; ++i) off[i] = tbase + (uint32_t)((i ^ l15) << 2);
+  for (int q = 0; q < M / 2; ++q)
+    xo[q] = (cpo + (uint32_t)(((2 * q) ^ l15) << 2)) | ((cpo + (uint32_t)(((2 * q + 1) ^ l15) << 2)) << 8);
+  // the code byte of step i is byte ((i & 3) ^ rx) of word w'[i >> 2] = w[(i >> 2) ^ qx]
   const int qx = l15 >> 2, rx = l15 & 3;
-  uint32_t sel[4];  // byte permute selectors: byte ((k ^ rx)) of the word -> bits 15..8, zeros elsewhere
+  uint32_t sel[4];  // selector nibbles: byte 0 <- xo byte 4 + (i & 1), byte 1 <- code, bytes 2, 3 <- xo bytes 6, 7 (0)
 #pragma unroll
-  for (int k = 0; k < 4; ++k) sel[k] = 0x4404u | ((uint32_t)(k ^ rx) << 4);
+  for (int k = 0; k < 4; ++k) sel[k] = 0x7600u | ((uint32_t)(k ^ rx) << 4) | (4u + (uint32_t)(k & 1));
+  const char* tabc = reinterpret_cast<const char*>(tab);
   const uint4* crow = reinterpret_cast<const uint4*>(codes + (size_t)unit * code_cap * M);
   int32_t* out = scores + (size_t)unit * score_stride - s0;
   // the 4 code words of a slot read in the order w'[i] = w[i ^ qx] (per-lane byte offsets)
@@ -245,11 +252,7 @@ __global__ void __launch_bounds__(SCORE_THREADS, 2) pq_score_kernel(const uint8_
     for (int i = 0; i < 4; ++i) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w[i]) : "r"(slot + woff[i]));
     int32_t acc = 0;
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
-      int32_t v;
-      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(off[i] + __byte_perm(w[i >> 2], 0u, sel[i & 3])));
-      acc += v;
-    }
+    for (int i = 0; i < M; ++i) acc += *reinterpret_cast<const int32_t*>(tabc + __byte_perm(w[i >> 2], xo[i >> 1], sel[i & 3]));
     return acc;
   };
   auto emit = [&](int j, int32_t sc) {
