@@ -75,7 +75,8 @@ __device__ __forceinline__ int seg_stages(const Ranges& rg) { return (rg.e0 - rg
 #ifndef MD_TC_PF
 #define MD_TC_PF 0  // measured: 2 or 4 stages of L2 prefetch slow Llama verify 1.26 -> 1.41 ms
 #endif
-constexpr int PF = MD_TC_PF;  // stages prefetched into L2 ahead of the ring
+constexpr int PF = MD_TC_PF;
+  // stages prefetched into L2 ahead of the ring
 template <int NP>
 __device__ void produce(const AttnParams& p, const TmapSet& tm, const CUtensorMap* qmap, const Seg& sg,
                         const Ranges& rg, uint8_t* ring, uint8_t* qbuf, uint64_t* full, uint64_t* empty,
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int x = threadIdx.x;                      // TMEM lane: key of the tile / head-dim row of O^T
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     int it = 0, tt = 0, si = 0;
-    long long w_sf = 0, w_pe = 0, t_start = clock64();
+    long long w_sf = 0, w_pe = 0, w_epi = 0, t_start = clock64();
     long long* wsf = (p.trace && x == 0) ? &w_sf : nullptr;
     long long* wpe = (p.trace && x == 0) ? &w_pe : nullptr;
     long long sec[6] = {0, 0, 0, 0, 0, 0}, tsec = 0;
@@ -515,6 +516,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         TSEC(5)
       }
       // ---------------- segment epilogue: row sums over the 128 key lanes, O^T / l
+      const long long t_epi = prof ? clock64() : 0;
 #pragma unroll
       for (int r = 0; r < NP; ++r) {
         float l = lacc[r];
@@ -556,12 +558,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (!complete && p.fused_merge) finish_unit<D>(p, sg, pl, SM_THREADS, flag);
       bar128();  // red / mrow / crow reused by the next segment
+      if (prof) w_epi += clock64() - t_epi;
       ++si;
     }
     if (p.trace && x == 0) {
       trace_put(p, 12, w_sf);
       trace_put(p, 13, w_pe);
       trace_put(p, 14, clock64() - t_start);
+      trace_put(p, 7, w_epi);  // segment epilogues (row sums, O^T read, stores, split merge)
       trace_put(p, 6, globaltimer());  // softmax end (ns): the CTA's finish time
       for (int k = 0; k < 6; ++k) trace_put(p, k, sec[k]);
     }

@@ -43,12 +43,15 @@ torch.cuda.synchronize()
 md.debug_trace(None)
 t = trace.cpu().numpy().astype(np.float64)
 t = t[t[:, 11] > 0]
-names = {0: "sm_ld", 1: "sm_scale_need", 2: "sm_vote_rescale", 3: "sm_exp_pack", 4: "sm_pstore", 5: "sm_fence_arrive", 8: "mma_wait_full", 9: "mma_wait_sempty", 10: "mma_wait_pfull", 12: "sm_wait_sfull", 13: "sm_wait_pempty",
+names = {0: "sm_ld", 1: "sm_scale_need", 2: "sm_vote_rescale", 3: "sm_exp_pack", 4: "sm_pstore", 5: "sm_fence_arrive", 7: "sm_epilogue", 8: "mma_wait_full", 9: "mma_wait_sempty", 10: "mma_wait_pfull", 12: "sm_wait_sfull", 13: "sm_wait_pempty",
          14: "sm_total", 15: "prod_wait_empty"}
 res = {"cfg": cfg, "ctas": int(len(t)), "call_us": round(a.elapsed_time(b) * 1e3, 1),
        "tiles_per_cta": float(np.median(t[:, 11]))}
 for i, nme in names.items():
     res[nme + "_kcyc_p50"] = round(float(np.median(t[:, i])) / 1e3, 1)
+acc_cols = [0, 1, 2, 3, 4, 5, 7, 12, 13]
+res["sm_unaccounted_kcyc_p10_p50_p90"] = [round(float(x) / 1e3, 1) for x in
+                                          np.percentile(t[:, 14] - t[:, acc_cols].sum(1), [10, 50, 90])]
 ends = t[:, 6]
 res["finish_spread_us"] = [round(float(x), 1) for x in np.percentile((ends - ends.min()) / 1e3, [0, 10, 50, 90, 100])]
 print(json.dumps(res))
