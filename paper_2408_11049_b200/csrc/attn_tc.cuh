@@ -71,16 +71,57 @@ __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, long long*
 // stages of a segment: [lo*64, min(keys, hi*64)) in 128-key steps
 __device__ __forceinline__ int seg_stages(const Ranges& rg) { return (rg.e0 - rg.s0 + KT - 1) / KT; }
 
-// TMA producer (one thread): Q rows of the segment, then its K/V stages
+// TMA producer (one thread): Q rows of the segment, then its K/V stages.  K and V halves of a
+// stage have their own full / empty barriers: the K half is free once the tile's S^T MMAs
+// complete, the V half only after its PV, so the next K loads go out a whole softmax earlier.
+// The V half of tile i is issued after the K half of tile i + 1 (V is consumed one softmax
+// later than K), so a K load never waits behind the longer V release.
 #ifndef MD_TC_PF
 #define MD_TC_PF 0  // measured: 2 or 4 stages of L2 prefetch slow Llama verify 1.26 -> 1.41 ms
 #endif
-constexpr int PF = MD_TC_PF;
-  // stages prefetched into L2 ahead of the ring
+constexpr int PF = MD_TC_PF;  // stages prefetched into L2 ahead of the ring
+struct PendV {                // a V half not yet issued
+  int it, pos, nvalid, b, kvh;
+};
+__device__ __forceinline__ int half_bytes(int nvalid) {  // bytes of one K (or V) half
+  int bytes = 0;
+  for (int h = 0; h < 2; ++h) {
+    const int hv = nvalid - h * TK;
+    if (hv >= TK) bytes += 2 * TK * 128;
+    else if (hv > 0) bytes += 2 * ((hv + BOX_ROWS - 1) / BOX_ROWS) * BOX_ROWS * 128;
+  }
+  return bytes;
+}
+template <int NSTAGE>
+__device__ __forceinline__ void load_half(const CUtensorMap* full_map, const CUtensorMap* part_map, uint8_t* dst,
+                                          uint64_t* bar, int pos, int nvalid, int kvh, int b, uint64_t pol) {
+  for (int h = 0; h < 2; ++h) {
+    const int hv = nvalid - h * TK, r0 = pos + h * TK;
+    for (int sub = 0; sub < 2; ++sub) {
+      const int off = sub * SLAB + h * TK * 128;
+      if (hv >= TK) {
+        tma_load_4d(dst + off, full_map, bar, sub * 64, r0, kvh, b, pol);
+      } else if (hv > 0) {
+        for (int bx = 0; bx * BOX_ROWS < hv; ++bx)
+          tma_load_4d(dst + off + bx * BOX_ROWS * 128, part_map, bar, sub * 64, r0 + bx * BOX_ROWS, kvh, b, pol);
+      }
+    }
+  }
+}
+template <int NSTAGE>
+__device__ __forceinline__ void issue_v(const TmapSet& tm, uint8_t* ring, uint64_t* vfull, uint64_t* vempty,
+                                        const PendV& pv, uint64_t pol) {
+  const int stage = pv.it % NSTAGE;
+  mbar_wait(&vempty[stage], ((pv.it / NSTAGE) & 1) ^ 1);
+  mbar_arrive_expect_tx(&vfull[stage], half_bytes(pv.nvalid));
+  load_half<NSTAGE>(&tm.v_full, &tm.v_part, ring + stage * STAGE + 2 * SLAB, &vfull[stage], pv.pos, pv.nvalid, pv.kvh,
+                    pv.b, pol);
+}
 template <int NP>
 __device__ void produce(const AttnParams& p, const TmapSet& tm, const CUtensorMap* qmap, const Seg& sg,
                         const Ranges& rg, uint8_t* ring, uint8_t* qbuf, uint64_t* full, uint64_t* empty,
-                        uint64_t* qfull, uint64_t* qempty, int& it, int& qi, uint64_t pol, long long* tw) {
+                        uint64_t* vfull, uint64_t* vempty, uint64_t* qfull, uint64_t* qempty, int& it, int& qi,
+                        PendV& pend, uint64_t pol, long long* tw) {
   using C = Cfg<NP>;
   const int qs = qi % C::NQ;
   mbar_wait(&qempty[qs], ((qi / C::NQ) & 1) ^ 1);
@@ -91,18 +132,9 @@ __device__ void produce(const AttnParams& p, const TmapSet& tm, const CUtensorMa
   for (int pos = rg.s0; pos < rg.e0; pos += KT, ++it) {
     const int stage = it % C::NSTAGE;
     const int nvalid = min(KT, rg.e0 - pos);
-    uint8_t* kt = ring + stage * STAGE;
-    uint8_t* vt = kt + 2 * SLAB;
     twait(&empty[stage], ((it / C::NSTAGE) & 1) ^ 1, tw);
-    int bytes = 0;
-    for (int h = 0; h < 2; ++h) {
-      const int hv = nvalid - h * TK;
-      if (hv >= TK) bytes += 2 * 2 * TK * 128;
-      else if (hv > 0) bytes += 2 * 2 * ((hv + BOX_ROWS - 1) / BOX_ROWS) * BOX_ROWS * 128;
-    }
-    mbar_arrive_expect_tx(&full[stage], bytes);
-    // L2 prefetch PF stages ahead (full 64-row boxes only): deepens the memory pipeline beyond
-    // the shared-memory ring, which the consumers hold for a stage's S^T, softmax and PV
+    mbar_arrive_expect_tx(&full[stage], half_bytes(nvalid));
+    // L2 prefetch PF stages ahead (full 64-row boxes only)
     if (PF > 0) {
       const int pp = pos + PF * KT;
       for (int h = 0; h < 2; ++h) {
@@ -114,23 +146,9 @@ __device__ void produce(const AttnParams& p, const TmapSet& tm, const CUtensorMa
           }
       }
     }
-    for (int h = 0; h < 2; ++h) {
-      const int hv = nvalid - h * TK, r0 = pos + h * TK;
-      for (int sub = 0; sub < 2; ++sub) {
-        const int off = sub * SLAB + h * TK * 128;
-        if (hv >= TK) {
-          tma_load_4d(kt + off, &tm.k_full, &full[stage], sub * 64, r0, sg.kvh, sg.b, pol);
-          tma_load_4d(vt + off, &tm.v_full, &full[stage], sub * 64, r0, sg.kvh, sg.b, pol);
-        } else if (hv > 0) {
-          for (int bx = 0; bx * BOX_ROWS < hv; ++bx) {
-            tma_load_4d(kt + off + bx * BOX_ROWS * 128, &tm.k_part, &full[stage], sub * 64, r0 + bx * BOX_ROWS,
-                        sg.kvh, sg.b, pol);
-            tma_load_4d(vt + off + bx * BOX_ROWS * 128, &tm.v_part, &full[stage], sub * 64, r0 + bx * BOX_ROWS,
-                        sg.kvh, sg.b, pol);
-          }
-        }
-      }
-    }
+    load_half<C::NSTAGE>(&tm.k_full, &tm.k_part, ring + stage * STAGE, &full[stage], pos, nvalid, sg.kvh, sg.b, pol);
+    if (pend.it >= 0) issue_v<C::NSTAGE>(tm, ring, vfull, vempty, pend, pol);
+    pend = PendV{it, pos, nvalid, sg.b, sg.kvh};
   }
 }
 
@@ -159,7 +177,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* oempty = ofull + 2;      // [2]
   uint64_t* cfull = oempty + 2;      // [2] dynamic chunk hand-off, producer -> MMA + softmax
   uint64_t* cempty = cfull + 2;      // [2]
-  int* cids = reinterpret_cast<int*>(cempty + 2);  // [2]
+  uint64_t* vfull = cempty + 2;      // [NSTAGE] V halves of the ring stages (full / empty: K halves)
+  uint64_t* vempty = vfull + NSTAGE; // [NSTAGE]
+  int* cids = reinterpret_cast<int*>(vempty + NSTAGE);  // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(cids + 2);
   int* flag = reinterpret_cast<int*>(tslot + 4);                 // [16] finish_unit
   Plan* plan_smem = reinterpret_cast<Plan*>(flag + 16);          // 40 bytes (reserved 64)
@@ -173,6 +193,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&vfull[s], 1);
+      mbar_init(&vempty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&qfull[s], 1);
@@ -234,6 +256,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       prefetch_tmap(&qmap);
       const uint64_t pol = policy_evict_first();
       int it = 0, qi = 0, ck = 0;
+      PendV pend{-1, 0, 0, 0, 0};
       long long tw = 0;
       long long* twp = p.trace ? &tw : nullptr;
       // dynamic tail (long calls, see make_plan): chunks claimed one ahead from an atomic
@@ -256,8 +279,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
           continue;
         }
-        produce<NP>(p, tm, &qmap, sg, seg_ranges(p, sg), ring, qbuf, full, empty, qfull, qempty, it, qi, pol, twp);
+        produce<NP>(p, tm, &qmap, sg, seg_ranges(p, sg), ring, qbuf, full, empty, vfull, vempty, qfull, qempty, it, qi,
+                    pend, pol, twp);
       }
+      if (pend.it >= 0) issue_v<NSTAGE>(tm, ring, vfull, vempty, pend, pol);
       if (p.trace) trace_put(p, 15, tw);
     }
   } else if (warp == 5) {
@@ -271,8 +296,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       long long* ws_ = p.trace ? &w_se : nullptr;
       long long* wp = p.trace ? &w_pf : nullptr;
       // the PV of the previous tile is issued after this tile's S^T (S^T double-buffered)
-      int pv_stage = -1, pv_ob = 0, pv_first = 0, pv_last = 0, pv_qs = 0, pv_tt = 0;
+      int pv_stage = -1, pv_ob = 0, pv_first = 0, pv_last = 0, pv_qs = 0, pv_tt = 0, pv_it = 0;
       auto issue_pv = [&]() {
+        mbar_wait(&vfull[pv_stage], (pv_it / NSTAGE) & 1);
         twait(pfull, pv_tt & 1, wp);
         fence_after();
         const uint32_t vt = ring_a + pv_stage * STAGE + 2 * SLAB;
@@ -281,7 +307,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kk = 0; kk < KT / 16; ++kk)
           mma_f16(od, sdesc(vt + kk * 2048, SLAB, 1024, 2), sdesc(p_a + kk * 256, 128, 2048, 0), ID_O,
                   (pv_first && kk == 0) ? 0u : 1u);
-        commit(&empty[pv_stage]);
+        commit(&vempty[pv_stage]);
         commit(pempty);
         if (pv_last) commit(&ofull[pv_ob]);
         pv_stage = -1;
@@ -321,6 +347,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     kk > 0 ? 1u : 0u);
           }
           commit(&sfull[sb]);
+          commit(&empty[stage]);  // the K half is free once S^T is complete
           if (j == ns - 1) commit(&qempty[qs]);
           if (pv_stage >= 0) issue_pv();
           pv_stage = stage;
@@ -329,6 +356,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           pv_last = (j == ns - 1);
           pv_qs = qs;
           pv_tt = tt;
+          pv_it = it;
         }
         ++qi;
         ++si;
@@ -501,6 +529,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c = 0; c < NP / 8; ++c)
           *reinterpret_cast<uint4*>(pd + c * 2048) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         if (!valid) {  // zero this key's V row (cache rows past the valid keys may hold NaN bits)
+          mbar_wait(&vfull[stage], (it / NSTAGE) & 1);  // after the V half's TMA writes land
           uint8_t* vrow = ring + stage * STAGE + 2 * SLAB + x * 128;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
