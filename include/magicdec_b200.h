@@ -181,6 +181,21 @@ MD_API md_status md_draft_attn_sparse(const md_kv_cache* cache, const void* q, i
                                size_t workspace_bytes, md_stream_t stream);
 
 /*
+ * md_draft_attn_sparse_windows — md_draft_attn_sparse with a window per sequence, for
+ * heterogeneous batches ("different sequences in the same batch can leverage different draft
+ * KV cache sizes").  Sequence b attends to
+ *     J_b = {j < min(sink, n)}  U  {max(sink, n - w_b) <= j < n},
+ *     w_b = min(window, max(windows[b], max(0, 1 - sink)))    (n = kv_len[b]).
+ *   windows: device int32 [B]; `window` bounds every w_b and sizes the workspace exactly as
+ *   for md_draft_attn_sparse.  Other arguments, layouts and errors as md_draft_attn_sparse;
+ *   a NULL `windows` is MD_ERR_INVALID_ARG.
+ */
+MD_API md_status md_draft_attn_sparse_windows(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                              const int32_t* kv_len, int32_t sink, int32_t window,
+                                              const int32_t* windows, float scale, float* out, float* lse,
+                                              void* workspace, size_t workspace_bytes, md_stream_t stream);
+
+/*
  * md_draft_attn_indexed — self-speculative draft attention over a static SnapKV-selected KV
  * (the paper's best drafter; SnapKV with observation
  * window 32 and average pooling 5; per-sequence budgets).
@@ -211,14 +226,17 @@ MD_API md_status md_draft_attn_indexed(const md_kv_cache* cache, const void* q, 
  *   S1 a[hh,i,j] = softmax_j(scale q . k[b][u][j]) over the causal keys j <= L-w+i;
  *   S2 vote[j]   = sum_{hh,i} a[hh,i,j]                 for j < L-w;
  *   S3 pooled[j] = (vote[j-2] + ... + vote[j+2]) / 5     (zero padding);
- *   S4 idx[b][u][0 .. c) = the c = min(budget-w, L-w) largest pooled positions (ties ->
+ *   S4 idx[b][u][0 .. c) = the c = min(B_b-w, L-w) largest pooled positions (ties ->
  *      lower position), ascending; idx_count[b] = c.  Entries past c are left untouched.
+ *      B_b = budget, or with per-sequence budgets (heterogeneous batches)
+ *      B_b = min(max(budgets[b], w), budget).
  * The draft then attends to idx U [L-w, n) (pass tail_start = L - w).  Scores are fp32 on
  * the tensor cores, so positions whose pooled votes tie to ~1e-6 relative may order
  * differently from an fp64 evaluation.
  *   q_obs: device bf16 [B][w][Hq][head_dim]; prefill_len: device int32[B];
  *   max_prefill_len: host bound >= every prefill_len[b];
  *   idx: device int32 [B][Hkv][idx_stride] (idx_stride >= budget - w); idx_count: int32[B];
+ *   budgets: optional device int32[B] (NULL: every sequence uses `budget`, which bounds them);
  *   workspace: >= md_snapkv_workspace_bytes(B, Hq, Hkv, w, max_prefill_len) bytes (no init).
  * Supported: head_dim in {64, 128}, g*w <= 256.
  * Preconditions (device): w <= prefill_len[b] <= max_prefill_len.
@@ -227,7 +245,8 @@ MD_API size_t md_snapkv_workspace_bytes(int32_t batch, int32_t num_q_heads, int3
                                         int32_t max_prefill_len);
 MD_API md_status md_snapkv_select(const md_kv_cache* cache, const void* q_obs, int32_t num_q_heads,
                                   const int32_t* prefill_len, int32_t max_prefill_len, int32_t w, int32_t budget,
-                                  float scale, int32_t* idx, int32_t idx_stride, int32_t* idx_count, void* workspace,
+                                  const int32_t* budgets, float scale, int32_t* idx, int32_t idx_stride,
+                                  int32_t* idx_count, void* workspace,
                                   size_t workspace_bytes, md_stream_t stream);
 
 /*

@@ -70,7 +70,9 @@ def draft_index_set(n: int, sink: int, window: int) -> np.ndarray:
 
 
 def draft_attn_sparse(q_bits, k_cache_bits, v_cache_bits, kv_len, sink, window, scale):
-    """O3.  q_bits [B, Hq, d] uint16 -> out [B, Hq, d] fp64, lse [B, Hq] fp64."""
+    """O3.  q_bits [B, Hq, d] uint16 -> out [B, Hq, d] fp64, lse [B, Hq] fp64.  `window` may be a
+    per-sequence array [B] (heterogeneous batches: "different sequences in the same batch can
+    leverage different draft KV cache sizes")."""
     q = bf16_to_f64(q_bits)
     B, Hq, d = q.shape
     Hkv = k_cache_bits.shape[1]
@@ -78,7 +80,7 @@ def draft_attn_sparse(q_bits, k_cache_bits, v_cache_bits, kv_len, sink, window, 
     out = np.zeros((B, Hq, d))
     lse = np.zeros((B, Hq))
     for b in range(B):
-        J = draft_index_set(int(kv_len[b]), sink, window)
+        J = draft_index_set(int(kv_len[b]), sink, int(window[b]) if np.ndim(window) else window)
         for kvh in range(Hkv):
             K = bf16_to_f64(k_cache_bits[b, kvh, J])
             V = bf16_to_f64(v_cache_bits[b, kvh, J])

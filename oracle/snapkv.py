@@ -59,10 +59,12 @@ def topk_positions(pooled: np.ndarray, k: int) -> np.ndarray:
     return np.sort(order[:k]).astype(np.int32)
 
 
-def snapkv_select(q_obs_bits, k_cache_bits, prefill_len, w: int, budget: int, scale: float):
+def snapkv_select(q_obs_bits, k_cache_bits, prefill_len, w: int, budget: int, scale: float, budgets=None):
     """Batched S1-S4.  q_obs_bits [B, w, Hq, d] (queries of the last w prompt positions),
     k_cache_bits [B, Hkv, cap, d], prefill_len [B] ->
-    (idx [B, Hkv, budget - w] int32 (ascending; -1 padded), count [B] int32, pooled list)."""
+    (idx [B, Hkv, budget - w] int32 (ascending; -1 padded), count [B] int32, pooled list).
+    budgets: optional per-sequence budgets [B] ("different sequences in the same batch can
+    leverage different draft KV cache sizes"), each clamped to [w, budget]."""
     B, _, Hq, d = q_obs_bits.shape
     Hkv = k_cache_bits.shape[1]
     g = Hq // Hkv
@@ -72,7 +74,8 @@ def snapkv_select(q_obs_bits, k_cache_bits, prefill_len, w: int, budget: int, sc
     pooled_all = []
     for b in range(B):
         L = int(prefill_len[b])
-        cnt = min(kmax, L - w)
+        kb = kmax if budgets is None else min(max(int(budgets[b]), w), budget) - w
+        cnt = min(kb, L - w)
         count[b] = cnt
         row = []
         for h in range(Hkv):

@@ -30,7 +30,7 @@ ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_works
                "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace",
                "md_verify_attn_tree", "md_spec_accept_tree", "md_kv_compact", "md_pq_encode", "md_pq_workspace_bytes",
                "md_pq_select", "md_verify_attn_full_tp", "md_draft_attn_sparse_tp", "md_tp_barrier",
-               "md_philox_u32_dev")
+               "md_philox_u32_dev", "md_draft_attn_sparse_windows")
 
 
 class MDError(RuntimeError):
@@ -82,11 +82,13 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                         c_void_p, sz, c_void_p]
     lib.md_draft_attn_sparse.argtypes = [pc, c_void_p, i32, c_void_p, i32, i32, f32, c_void_p, c_void_p,
                                          c_void_p, sz, c_void_p]
+    lib.md_draft_attn_sparse_windows.argtypes = [pc, c_void_p, i32, c_void_p, i32, i32, c_void_p, f32, c_void_p,
+                                                 c_void_p, c_void_p, sz, c_void_p]
     lib.md_draft_attn_indexed.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, i32, c_void_p, c_void_p, f32,
                                           c_void_p, c_void_p, c_void_p, sz, c_void_p]
     lib.md_snapkv_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
     lib.md_snapkv_workspace_bytes.restype = sz
-    lib.md_snapkv_select.argtypes = [pc, c_void_p, i32, c_void_p, i32, i32, i32, f32, c_void_p, i32, c_void_p,
+    lib.md_snapkv_select.argtypes = [pc, c_void_p, i32, c_void_p, i32, i32, i32, c_void_p, f32, c_void_p, i32, c_void_p,
                                      c_void_p, sz, c_void_p]
     lib.md_philox_u32.argtypes = [u64, u64, i32, i32, c_void_p, c_void_p]
     lib.md_spec_accept.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, i32, i32, i32, ctypes.c_int,
@@ -112,7 +114,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     for name in ("md_kv_append", "md_verify_attn_full", "md_draft_attn_sparse", "md_draft_attn_indexed",
                  "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace", "md_verify_attn_tree",
                  "md_spec_accept_tree", "md_kv_compact", "md_pq_encode", "md_pq_select", "md_verify_attn_full_tp",
-                 "md_draft_attn_sparse_tp", "md_tp_barrier", "md_philox_u32_dev"):
+                 "md_draft_attn_sparse_tp", "md_tp_barrier", "md_philox_u32_dev", "md_draft_attn_sparse_windows"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -189,11 +191,18 @@ def verify_attn_tree(q, k_cache, v_cache, kv_len, max_kv_len, tree_mask, scale, 
                                    _ptr(tree_mask), float(scale), _ptr(out), _ptr(lse), ws, wsb, _stream(stream)))
 
 
-def draft_attn_sparse(q, k_cache, v_cache, kv_len, sink, window, scale, out, lse=None, workspace=None, stream=None):
-    """q [B, Hq, d] bf16 over the sink + window rows -> out [B, Hq, d] fp32 (and lse [B, Hq])."""
+def draft_attn_sparse(q, k_cache, v_cache, kv_len, sink, window, scale, out, lse=None, workspace=None, stream=None,
+                      windows=None):
+    """q [B, Hq, d] bf16 over the sink + window rows -> out [B, Hq, d] fp32 (and lse [B, Hq]).
+    windows: optional int32 [B] device tensor of per-sequence windows (each <= window)."""
     lib = load_library()
     c = make_cache(k_cache, v_cache)
     ws, wsb = _ws(workspace)
+    if windows is not None:
+        _check(lib.md_draft_attn_sparse_windows(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(kv_len), int(sink),
+                                                int(window), _ptr(windows), float(scale), _ptr(out), _ptr(lse), ws,
+                                                wsb, _stream(stream)))
+        return
     _check(lib.md_draft_attn_sparse(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(kv_len), int(sink), int(window),
                                     float(scale), _ptr(out), _ptr(lse), ws, wsb, _stream(stream)))
 
@@ -215,9 +224,10 @@ def snapkv_workspace_bytes(batch, num_q_heads, num_kv_heads, w, max_prefill_len)
 
 
 def snapkv_select(k_cache, v_cache, q_obs, prefill_len, max_prefill_len, w, budget, scale, idx, idx_count,
-                  workspace=None, stream=None):
+                  workspace=None, stream=None, budgets=None):
     """SnapKV selection at prefill: q_obs [B, w, Hq, d] bf16 -> idx [B, Hkv, K] int32 (ascending
-    positions, K >= budget - w), idx_count [B] int32."""
+    positions, K >= budget - w), idx_count [B] int32.  budgets: optional [B] int32 device tensor
+    of per-sequence budgets (each clamped to [w, budget])."""
     lib = load_library()
     c = make_cache(k_cache, v_cache)
     if workspace is None:
@@ -225,7 +235,8 @@ def snapkv_select(k_cache, v_cache, q_obs, prefill_len, max_prefill_len, w, budg
                                                        max_prefill_len), dtype=torch.uint8, device=q_obs.device)
     ws, wsb = _ws(workspace)
     _check(lib.md_snapkv_select(ctypes.byref(c), _ptr(q_obs), q_obs.shape[2], _ptr(prefill_len), int(max_prefill_len),
-                                int(w), int(budget), float(scale), _ptr(idx), idx.shape[2], _ptr(idx_count), ws, wsb,
+                                int(w), int(budget), _ptr(budgets) if budgets is not None else None, float(scale),
+                                _ptr(idx), idx.shape[2], _ptr(idx_count), ws, wsb,
                                 _stream(stream)))
 
 

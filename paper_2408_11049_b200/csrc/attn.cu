@@ -86,16 +86,23 @@ struct AttnParams {
   float* const* out_peers;
   int tp_world, out_hq, out_h0;
   int pdl_early;          // tcgen05 kernel: trigger the dependent launch at entry (1) or at exit (0)
+  const int32_t* windows; // MODE_DRAFT: per-sequence windows [B] or nullptr (p.window for all)
   int mode;
   float scale_log2;       // scale * log2(e)
 };
 
 // ------------------------------------------------------------------ stream-K decomposition
+// StreamingLLM window of sequence b: p.window, or its own (heterogeneous batches: "different
+// sequences in the same batch can leverage different draft KV cache sizes"), clamped
+// to [max(0, 1 - sink), p.window] so every sequence attends to at least one key
+__device__ __forceinline__ int window_of(const AttnParams& p, int b) {
+  return p.windows ? min(p.window, max(max(0, 1 - p.sink), __ldg(p.windows + b))) : p.window;
+}
 __device__ __forceinline__ int unit_keys(const AttnParams& p, int n, int b) {
   if (p.mode == MODE_VERIFY) return n;
   if (p.mode == MODE_INDEXED) return __ldg(p.idx_count + b) + max(0, n - __ldg(p.tail_start + b));
   const int nA = min(p.sink, n);
-  return nA + max(0, n - max(p.sink, n - p.window));
+  return nA + max(0, n - max(p.sink, n - window_of(p, b)));
 }
 __device__ __forceinline__ int unit_tiles(const AttnParams& p, int b) {
   return (unit_keys(p, __ldg(p.kv_len + b), b) + TK - 1) / TK;
@@ -273,7 +280,7 @@ __device__ __forceinline__ Ranges seg_ranges(const AttnParams& p, const Seg& sg)
     r.e1 = max(r.s1, tail + (hi - cnt));
   } else {
     const int nA = min(p.sink, sg.n);
-    const int startB = max(p.sink, sg.n - p.window);
+    const int startB = max(p.sink, sg.n - window_of(p, sg.b));
     r.e0 = max(lo, min(hi, nA));         // sink rows
     r.s1 = startB + (max(lo, nA) - nA);  // window rows
     r.e1 = max(r.s1, startB + (hi - nA));
@@ -1532,6 +1539,7 @@ struct IndexedArgs {
   const int32_t* tail_start = nullptr;
   const uint32_t* tree_mask = nullptr;  // verify only
   const md_tp_out* tp = nullptr;        // f1: outputs stored into every TP rank's full-head buffer
+  const int32_t* windows = nullptr;     // draft: per-sequence windows
 };
 
 static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int T, const int32_t* kv_len, int sink,
@@ -1596,6 +1604,7 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.idx_count = ix.idx_count;
   p.tail_start = ix.tail_start;
   p.tree_mask = ix.tree_mask;
+  p.windows = ix.windows;
   p.out_peers = ix.tp ? ix.tp->out_peers : nullptr;
   p.tp_world = ix.tp ? ix.tp->world : 1;
   p.out_hq = ix.tp ? ix.tp->world * Hq : Hq;
@@ -1696,6 +1705,22 @@ extern "C" md_status md_draft_attn_sparse(const md_kv_cache* cache, const void* 
              "md_draft_attn_sparse: need sink >= 0, window >= 0, sink + window >= 1");
   return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, out, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse");
+}
+
+extern "C" md_status md_draft_attn_sparse_windows(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                                  const int32_t* kv_len, int32_t sink, int32_t window,
+                                                  const int32_t* windows, float scale, float* out, float* lse,
+                                                  void* workspace, size_t workspace_bytes, md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(cache != nullptr && windows != nullptr, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_windows: NULL cache / windows");
+  MD_REQUIRE(sink >= 0 && window >= 0 && (int64_t)sink + window >= 1, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_windows: need sink >= 0, window >= 0, sink + window >= 1");
+  IndexedArgs ix;
+  ix.windows = windows;
+  return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, out, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_windows", ix);
 }
 
 extern "C" md_status md_draft_attn_indexed(const md_kv_cache* cache, const void* q, int32_t num_q_heads,

@@ -50,6 +50,7 @@ struct Params {
   int32_t* idx;            // [B][Hkv][idx_stride]
   int32_t* idx_count;      // [B]
   int idx_stride, keep;    // keep = budget - w
+  const int32_t* budgets;  // [B] per-sequence budgets or nullptr
 };
 
 // cooperative swizzled load of KT keys x D (bf16) of one unit into smem (zero rows past nkeys)
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const Params p) {
   __shared__ uint32_t hist[256];
   __shared__ uint32_t scan_sm[SEL_THREADS / 32];
   __shared__ uint32_t s_prefix, s_need;
+  __shared__ int s_keep;
   pdl_trigger();
   pdl_wait();
   const int unit = blockIdx.x;
@@ -331,8 +333,16 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const Params p) {
   int32_t* out = p.idx + ((int64_t)b * p.Hkv + h) * p.idx_stride;
   const float* vote = p.vote + (int64_t)unit * p.maxL;
   float* pooled = p.pooled + (int64_t)unit * p.maxL;
-  const int keep = max(0, min(p.keep, n));
-  if (h == 0 && threadIdx.x == 0) p.idx_count[b] = keep;
+  // per-sequence budget (heterogeneous batches): clamped to [w, budget]; read by one
+  // thread and broadcast through shared memory
+  if (threadIdx.x == 0) {
+    int kb = p.keep;
+    if (p.budgets != nullptr) kb = min(kb, max(0, p.budgets[b] - p.w));
+    s_keep = max(0, min(kb, n));
+    if (h == 0) p.idx_count[b] = s_keep;
+  }
+  __syncthreads();
+  const int keep = s_keep;
   if (keep == n) {  // budget covers the prompt: keep everything
     for (int j = threadIdx.x; j < n; j += SEL_THREADS) out[j] = j;
     return;
@@ -729,7 +739,8 @@ extern "C" MD_API size_t md_snapkv_workspace_bytes(int32_t batch, int32_t num_q_
 
 extern "C" MD_API md_status md_snapkv_select(const md_kv_cache* c, const void* q_obs, int32_t num_q_heads,
                                       const int32_t* prefill_len, int32_t max_prefill_len, int32_t w, int32_t budget,
-                                      float scale, int32_t* idx, int32_t idx_stride, int32_t* idx_count,
+                                      const int32_t* budgets, float scale, int32_t* idx, int32_t idx_stride,
+                                      int32_t* idx_count,
                                       void* workspace, size_t workspace_bytes, md_stream_t stream) {
   using namespace md;
   clear_error();
@@ -777,6 +788,7 @@ extern "C" MD_API md_status md_snapkv_select(const md_kv_cache* c, const void* q
   p.idx_count = idx_count;
   p.idx_stride = idx_stride;
   p.keep = budget - w;
+  p.budgets = budgets;
   cudaStream_t s = (cudaStream_t)stream;
   const unsigned grid = static_cast<unsigned>(units * p.nchunks);
   if (c->head_dim == 128 && snap_tc_enabled()) {

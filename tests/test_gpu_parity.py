@@ -6,6 +6,7 @@ Tolerances (north_star): attention outputs max-abs <= 2e-3, lse <
 Shapes: shrunken variants of every BASELINE.json config (same head geometry, smaller
 B / ctx) that span several 64-key tiles, several splits and a ragged tail.
 """
+import ctypes
 import zlib
 
 import numpy as np
@@ -143,6 +144,32 @@ def test_draft_peaky():
     o, l = _run_draft(case, 4, 1020)
     ro, rl = OA.draft_attn_sparse(case.qd_bits, case.k_bits, case.v_bits, case.kv_len, 4, 1020, case.scale)
     _cmp(o, l, ro, rl)
+
+
+@pytest.mark.parametrize("sink", [4, 0])
+def test_draft_per_sequence_windows(sink):
+    """md_draft_attn_sparse_windows: per-sequence windows, clamped to [max(0, 1 - sink),
+    window]; covers window 0, a window covering the sequence, one above the bound and ragged
+    lengths spanning several tiles."""
+    lens = [4000, 1500, 700, 90, 3000, 2]
+    windows = [1020, 0, 64, 500, 5000, 1]
+    B, Hq, Hkv, d, window = len(lens), 32, 8, 128, 1020
+    case = AttnCase(B, Hq, Hkv, d, max(lens) + 3, lens, seed=41 + sink).to_cuda()
+    out = torch.full((B, Hq, d), float("nan"), device="cuda")
+    lse = torch.full((B, Hq), float("nan"), device="cuda")
+    ws = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, 1, sink + window), dtype=torch.uint8, device="cuda")
+    wt = torch.tensor(windows, dtype=torch.int32, device="cuda")
+    md.draft_attn_sparse(case.qd, case.k, case.v, case.kv_len_t, sink, window, case.scale, out, lse, ws, windows=wt)
+    torch.cuda.synchronize()
+    eff = np.minimum(window, np.maximum(np.array(windows), max(0, 1 - sink)))
+    ro, rl = OA.draft_attn_sparse(case.qd_bits, case.k_bits, case.v_bits, case.kv_len, sink, eff, case.scale)
+    _cmp(out.cpu().numpy(), lse.cpu().numpy(), ro, rl)
+    # a NULL windows pointer is rejected on the host
+    lib = md.load_library()
+    c = md.make_cache(case.k, case.v)
+    st = lib.md_draft_attn_sparse_windows(ctypes.byref(c), case.qd.data_ptr(), Hq, case.kv_len_t.data_ptr(), sink,
+                                          window, None, 0.1, out.data_ptr(), None, ws.data_ptr(), ws.numel(), None)
+    assert st != 0 and b"windows" in lib.md_last_error()
 
 
 def test_kv_append_bit_exact():

@@ -130,6 +130,27 @@ def test_snapkv_select_matches_oracle(B, Hq, Hkv, d, L, w, budget, regime):
     _check_selection(idx.cpu().numpy(), cnt.cpu().numpy(), ref_idx, ref_cnt, pooled)
 
 
+def test_snapkv_select_per_sequence_budgets():
+    """Per-sequence budgets (heterogeneous batches): budgets below w keep nothing,
+    above `budget` are clamped to it; each sequence's list matches the oracle's."""
+    import synth as S
+    B, Hq, Hkv, d, w, budget = 4, 32, 8, 128, 32, 512
+    L = [3000, 2100, 1500, 900]
+    budgets = [100, 10, 4096, 2048]
+    reg = S.Regime("peaky", sink=4, needle_period=97)
+    case = AttnCase(B, Hq, Hkv, d, max(L) + 8, L, seed=77, regime=reg).to_cuda()
+    q_obs_bits = k_to_bf16_bits(S.q_rows_k(81, S.T_QVERIFY, B, w, Hq, Hkv, d, regime=reg))
+    idx = torch.full((B, Hkv, budget - w), -1, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(B, dtype=torch.int32, device="cuda")
+    md.snapkv_select(case.k, case.v, bits_to_torch_bf16(q_obs_bits), torch.tensor(L, dtype=torch.int32).cuda(),
+                     max(L), w, budget, case.scale, idx, cnt, budgets=torch.tensor(budgets, dtype=torch.int32).cuda())
+    torch.cuda.synchronize()
+    ref_idx, ref_cnt, pooled = SK.snapkv_select(q_obs_bits, case.k_bits, np.array(L), w, budget, case.scale,
+                                                budgets=np.array(budgets))
+    assert cnt.cpu().tolist() == ref_cnt.tolist() == [100 - w, 0, budget - w, budget - w]
+    _check_selection(idx.cpu().numpy(), cnt.cpu().numpy(), ref_idx, ref_cnt, pooled)
+
+
 def test_snapkv_select_mma_sync_path():
     """The mma.sync passes (MD_SNAP_TC=0; also every head_dim-64 call) on the d=128 cases."""
     import os

@@ -148,6 +148,24 @@ def test_draft_equals_attention_over_gathered_rows():
         assert np.max(np.abs(o[b] - ref[0, 0])) < 1e-12
 
 
+def test_draft_per_sequence_windows():
+    """Per-sequence windows: a covering window gives full attention for that sequence
+    only, and every sequence matches an SDPA over its own materialised sink + window rows."""
+    rng = np.random.default_rng(13)
+    B, Hq, Hkv, d, cap = 3, 4, 2, 64, 200
+    qb, kb, vb = _bits(rng, (B, Hq, d)), _bits(rng, (B, Hkv, cap, d)), _bits(rng, (B, Hkv, cap, d))
+    kv_len = np.array([200, 150, 120])
+    windows = np.array([196, 10, 50])
+    o, lse = A.draft_attn_sparse(qb, kb, vb, kv_len, 4, windows, 0.125)
+    full, lfull = A.verify_attn_full(qb[:, None], kb, vb, kv_len, 0.125)
+    assert np.array_equal(o[0], full[0, 0]) and np.array_equal(lse[0], lfull[0, 0])
+    assert np.max(np.abs(o[1] - full[1, 0])) > 1e-3   # a short window really drops keys
+    for b in range(B):
+        J = [j for j in range(kv_len[b]) if j < 4 or j >= kv_len[b] - windows[b]]
+        ref = _sdpa_verify(qb[b:b + 1, None], kb[b:b + 1, :, J], vb[b:b + 1, :, J], np.array([len(J)]), 0.125)
+        assert np.max(np.abs(o[b] - ref[0, 0])) < 1e-12
+
+
 def test_split_merge_identity():
     rng = np.random.default_rng(12)
     n, d = 300, 32

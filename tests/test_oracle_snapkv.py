@@ -90,3 +90,27 @@ def test_indexed_draft_with_full_prefix_is_full_attention():
     o, l = SK.draft_attn_indexed(case.qd_bits, case.k_bits, case.v_bits, case.kv_len, idx, tail, tail, case.scale)
     ro, rl = OA.verify_attn_full(case.qd_bits[:, None], case.k_bits, case.v_bits, case.kv_len, case.scale)
     assert np.array_equal(o, ro[:, 0]) and np.array_equal(l, rl[:, 0])
+
+
+def test_per_sequence_budgets():
+    """Heterogeneous batches: sequence b keeps min(clamp(budgets[b], w, budget) - w,
+    L - w) positions.  Pinned by the needle case (exact set), by clamping at both ends, and by
+    equality with the uniform-budget selection at each sequence's own budget."""
+    B, Hq, Hkv, d, L, w = 3, 4, 2, 16, 200, 8
+    rng = np.random.default_rng(1)
+    qk = rng.integers(-2, 3, size=(B, w, Hq, d))
+    kk = rng.integers(-2, 3, size=(B, Hkv, L, d))
+    direction = np.sign(rng.standard_normal(d)).astype(int)
+    qk = qk + 20 * direction
+    kk[:, :, 77] = 40 * direction
+    qb, kb = k_to_bf16_bits(qk), k_to_bf16_bits(kk)
+    budget = w + 40
+    idx, cnt, _ = SK.snapkv_select(qb, kb, np.full(B, L), w, budget, 0.25, budgets=np.array([w + 5, 3, 10 ** 6]))
+    assert cnt.tolist() == [5, 0, 40]
+    for h in range(Hkv):
+        assert idx[0, h, :5].tolist() == [75, 76, 77, 78, 79]
+        assert (idx[1, h] == -1).all()
+    for b, bud in ((0, w + 5), (2, budget)):
+        ref, rc, _ = SK.snapkv_select(qb[b:b + 1], kb[b:b + 1], np.array([L]), w, bud, 0.25)
+        assert rc[0] == cnt[b]
+        assert np.array_equal(ref[0, :, :rc[0]], idx[b, :, :cnt[b]])
