@@ -202,7 +202,7 @@ MD_API md_status md_draft_attn_sparse_windows(const md_kv_cache* cache, const vo
  * For b < B, h < Hq, with n = kv_len[b], kv head u = h / g:
  *     J = {idx[b][u][i] : i < idx_count[b]}  U  {tail_start[b] <= j < n}
  *     out[b][h][:] = softmax_j(scale * q[b][h] . k[b][u][j]) @ v[b][u][J],  lse likewise.
- * The listed rows are gathered from the shared cache in place (TMA tile::gather4), the tail
+ * The listed rows are copied from the shared cache in place (16-byte cp.async per row), the tail
  * (the observation window plus every token generated since prefill) is streamed.
  *   idx: device int32 [B][Hkv][idx_stride], 16-byte aligned, idx_stride % 4 == 0; entries
  *        0 <= idx < tail_start[b] (ascending order recommended for locality).

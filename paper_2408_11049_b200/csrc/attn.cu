@@ -47,10 +47,10 @@ constexpr float LN2 = 0.6931471805599453f;
 
 enum : int { MODE_VERIFY = 0, MODE_DRAFT = 1, MODE_INDEXED = 2 };
 
-// K and V tensor maps with a full-tile box (TK rows) and a partial-tile box (BOX_ROWS rows);
-// for the index-list draft also 2-D row views of K and V for tile::gather4.
+// K and V tensor maps with a full-tile box (TK rows) and a partial-tile box (BOX_ROWS rows)
+// (the index-list draft copies its listed rows with cp.async: no row maps)
 struct TmapSet {
-  CUtensorMap k_full, v_full, k_part, v_part, k_rows, v_rows;
+  CUtensorMap k_full, v_full, k_part, v_part;
 };
 
 constexpr int XS_FRAGS = 3;  // rows kernel: at most MT * (KS - 1) = 3 parked warp fragments per CTA
@@ -332,7 +332,7 @@ __device__ __forceinline__ void store_out(const AttnParams& p, int64_t off, V v)
 // ------------------------------------------------------------------ producer
 // Stream the K/V tiles of one segment into the ring; `it` is the running tile counter.
 // Called by all 32 lanes of the producer warp (lane 0 owns the barriers; in MODE_INDEXED
-// lanes 0..15 each gather 4 listed rows of an index-list tile with tile::gather4).
+// every lane copies 2 listed rows of an index-list tile with cp.async).
 template <int D, int NSTAGE>
 __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapSet& tm, const Ranges& rg, int b,
                                                 int kvh, uint8_t* ring, uint64_t* full, uint64_t* empty, int& it,
@@ -592,10 +592,6 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
       prefetch_tmap(&tm.v_full);
       prefetch_tmap(&tm.k_part);
       prefetch_tmap(&tm.v_part);
-      if (p.mode == MODE_INDEXED) {
-        prefetch_tmap(&tm.k_rows);
-        prefetch_tmap(&tm.v_rows);
-      }
     }
     const uint64_t pol = policy_evict_first();
     int it = 0, ck = 0;
@@ -995,10 +991,6 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       prefetch_tmap(&tm.v_full);
       prefetch_tmap(&tm.k_part);
       prefetch_tmap(&tm.v_part);
-      if (p.mode == MODE_INDEXED) {
-        prefetch_tmap(&tm.k_rows);
-        prefetch_tmap(&tm.v_rows);
-      }
     }
     const uint64_t pol = policy_evict_first();
     int it = 0, qi = 0, ck = 0;
@@ -1425,25 +1417,6 @@ static md_status make_tmap(CUtensorMap* m, const md_kv_cache* c, void* base, int
   return MD_OK;
 }
 
-// 2-D view of a cache as rows of d elements (row = b*row_sB + h*row_sH + pos*row_sS), box
-// {64 columns, 1 row} with SWIZZLE_128B, for tile::gather4 of listed rows.
-static md_status make_row_tmap(CUtensorMap* m, const md_kv_cache* c, void* base) {
-  auto enc = get_encode();
-  MD_REQUIRE(enc != nullptr, MD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
-  const int64_t d = c->head_dim;
-  const int64_t rows = (c->batch - 1) * (c->stride_b / d) + (c->num_kv_heads - 1) * (c->stride_h / d) +
-                       (c->capacity - 1) * (c->stride_s / d) + 1;
-  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-  cuuint32_t box[2] = {64, 1};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  MD_REQUIRE(r == CUDA_SUCCESS, MD_ERR_INVALID_ARG, "cuTensorMapEncodeTiled (row view) failed (code %d)", (int)r);
-  return MD_OK;
-}
-
 template <typename K>
 static md_status set_smem(K kern, int bytes, int* done_dev) {
   int dev = 0;
@@ -1578,11 +1551,6 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
     MD_REQUIRE(R <= 8, MD_ERR_UNSUPPORTED, "%s: at most 8 query heads per KV head", who);
     MD_REQUIRE(c->stride_s % c->head_dim == 0 && c->stride_h % c->head_dim == 0 && c->stride_b % c->head_dim == 0,
                MD_ERR_UNSUPPORTED, "%s: cache strides must be multiples of head_dim for row gathers", who);
-    if ((st = make_row_tmap(&tm.k_rows, c, c->k)) != MD_OK || (st = make_row_tmap(&tm.v_rows, c, c->v)) != MD_OK)
-      return st;
-  } else {
-    tm.k_rows = tm.k_full;  // unused
-    tm.v_rows = tm.v_full;
   }
   AttnParams p{};
   p.q = static_cast<const uint16_t*>(q);

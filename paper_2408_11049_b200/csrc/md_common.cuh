@@ -128,20 +128,6 @@ MD_DEV int atomic_add_acq_rel_gpu(int* p, int v) {
 }  // namespace md
 
 namespace md {
-// tile::gather4 (sm_100): 4 rows (coordinates r0..r3) x box-width columns of a 2-D tensor
-// map into consecutive smem rows, with the map's swizzle, completing on an mbarrier.
-MD_DEV void tma_gather4(void* dst, const void* tmap, uint64_t* bar, int col, int r0, int r1, int r2, int r3,
-                        uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
-      "l"(policy)
-      : "memory");
-}
-}  // namespace md
-
-namespace md {
 // L2 prefetch of a 4-D tensor tile (no smem, no mbarrier): raises memory-level parallelism
 // beyond the smem ring depth.
 MD_DEV void tma_prefetch_4d(const void* tmap, int c0, int c1, int c2, int c3) {
