@@ -231,12 +231,19 @@ def run_gpu(args):
         else:
             xv = xd = None
 
+    # a1 fused into a2/a3 (md_*_append): one launch per layer-call instead of append + attention
+    fused = not args.no_fused_append
+
     def layer_pass(pos):
         # pos[j] = committed + j  (rows: draft j start = pos[j], draft j kv_len = pos[j+1],
         #                          verify start = pos[0], verify kv_len = pos[gamma+1])
         for j in range(gamma):
             for l in range(layers):
                 kb, vb = kc[l % R], vc[l % R]
+                if fused and xd is None and world == 1:  # append fused into the draft call (one launch)
+                    md.draft_attn_sparse_append(qd, kb, vb, knew_d, vnew_d, pos[j + 1], sink, window, scale, out_d,
+                                                lse_d, ws_d)
+                    continue
                 md.kv_append(kb, vb, knew_d, vnew_d, pos[j])
                 if xd is not None:
                     md.draft_attn_sparse_tp(qd, kb, vb, pos[j + 1], sink, window, scale, xd.out, lse_d, ws_d)
@@ -247,6 +254,10 @@ def run_gpu(args):
                     gather_rank_major(out_d, gath_d)
         for l in range(layers):
             kb, vb = kc[l % R], vc[l % R]
+            if fused and xv is None and world == 1:  # append fused into the verify call (one launch)
+                md.verify_attn_full_append(qv, kb, vb, knew_v, vnew_v, pos[gamma + 1], max_kv, scale, out_v, lse_v,
+                                           ws_v)
+                continue
             md.kv_append(kb, vb, knew_v, vnew_v, pos[0])
             if xv is not None:
                 md.verify_attn_full_tp(qv, kb, vb, pos[gamma + 1], max_kv, scale, xv.out, lse_v, ws_v)
@@ -258,6 +269,8 @@ def run_gpu(args):
 
     # per layer-call: md_kv_append + one attention kernel (stream-K, merge fused); + philox + accept
     launches_per_step = gamma * layers * 2 + layers * 2 + 2
+    if fused and world == 1:
+        launches_per_step = gamma * layers + layers + 2
     if world > 1:
         launches_per_step += gamma * layers + layers  # the exchange after every attention call
 
@@ -359,12 +372,21 @@ def run_gpu(args):
         torch.cuda.synchronize()
         return a.elapsed_time(b_) / nrep
 
-    v_ms = time_calls(lambda r: md.verify_attn_full(qv, kc[r % R], vc[r % R], kv_len_v, max_kv, scale, out_v, lse_v,
-                                                    ws_v))
-    d_ms = time_calls(lambda r: md.draft_attn_sparse(qd, kc[r % R], vc[r % R], kv_len_d, sink, window, scale, out_d,
-                                                     lse_d, ws_d))
-    vb = verify_bytes(kvl_now, Hkv, Hq, d, T)
-    db = draft_bytes(kvl_now - T + 1, Hkv, Hq, d, sink, window)
+    # the kernels the step runs: with the fused append, the *_append calls (their algorithmic
+    # bytes add the new rows read from k_new / v_new and written to the cache: 4 B*T*Hkv*d*2)
+    fused_step = fused and world == 1
+    if fused_step:
+        v_ms = time_calls(lambda r: md.verify_attn_full_append(qv, kc[r % R], vc[r % R], knew_v, vnew_v, kv_len_v,
+                                                               max_kv, scale, out_v, lse_v, ws_v))
+        d_ms = time_calls(lambda r: md.draft_attn_sparse_append(qd, kc[r % R], vc[r % R], knew_d, vnew_d, kv_len_d,
+                                                                sink, window, scale, out_d, lse_d, ws_d))
+    else:
+        v_ms = time_calls(lambda r: md.verify_attn_full(qv, kc[r % R], vc[r % R], kv_len_v, max_kv, scale, out_v,
+                                                        lse_v, ws_v))
+        d_ms = time_calls(lambda r: md.draft_attn_sparse(qd, kc[r % R], vc[r % R], kv_len_d, sink, window, scale,
+                                                         out_d, lse_d, ws_d))
+    vb = verify_bytes(kvl_now, Hkv, Hq, d, T) + (4 * B * T * Hkv * d * 2 if fused_step else 0)
+    db = draft_bytes(kvl_now - T + 1, Hkv, Hq, d, sink, window) + (4 * B * Hkv * d * 2 if fused_step else 0)
     v_gbs, d_gbs = vb / v_ms / 1e6, db / d_ms / 1e6
     peak, peak_kind = load_peaks()
     traffic = None
@@ -445,14 +467,22 @@ def run_gpu(args):
                 if c < gamma * layers:
                     j = c // layers
                     q_, k_, v_ = st_d[sl]
-                    md.kv_append(kb, vb_, k_, v_, pos_buf[j])
-                    md.draft_attn_sparse(q_, kb, vb_, pos_buf[j + 1], sink, window, scale, out_d, lse_d, ws_d)
+                    if fused and world == 1:
+                        md.draft_attn_sparse_append(q_, kb, vb_, k_, v_, pos_buf[j + 1], sink, window, scale, out_d,
+                                                    lse_d, ws_d)
+                    else:
+                        md.kv_append(kb, vb_, k_, v_, pos_buf[j])
+                        md.draft_attn_sparse(q_, kb, vb_, pos_buf[j + 1], sink, window, scale, out_d, lse_d, ws_d)
                     if world > 1:
                         gather_rank_major(out_d, gath_d)
                 else:
                     q_, k_, v_ = st_v[sl]
-                    md.kv_append(kb, vb_, k_, v_, pos_buf[0])
-                    md.verify_attn_full(q_, kb, vb_, pos_buf[gamma + 1], max_kv, scale, out_v, lse_v, ws_v)
+                    if fused and world == 1:
+                        md.verify_attn_full_append(q_, kb, vb_, k_, v_, pos_buf[gamma + 1], max_kv, scale, out_v,
+                                                   lse_v, ws_v)
+                    else:
+                        md.kv_append(kb, vb_, k_, v_, pos_buf[0])
+                        md.verify_attn_full(q_, kb, vb_, pos_buf[gamma + 1], max_kv, scale, out_v, lse_v, ws_v)
                     if world > 1:
                         gather_rank_major(out_v, gath_v)
                 done[sl].record(cur)
@@ -511,13 +541,16 @@ def run_gpu(args):
                        "attention_only": True,
                        "cuda_graph": ("layer loop" if split else "whole step (drafts + verify + philox + accept)")
                        if use_graph else False,
+                       "kv_append": "fused into the attention calls" if fused and world == 1 else "separate launches",
                        "parallelism": (f"tp{world} (KV heads, {exchange} exchange)" if world > 1
                                        else "single GPU")},
             "tokens_per_step": round(tokens / args.steps, 3),
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "hbm", "achieved": round(v_gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(v_gbs / peak, 4), "traffic": traffic,
-                         "kernel": "md_verify_attn_full (attn_tc_kernel: tcgen05 MMAs with TMEM accumulators, stream-K persistent, fused split merge)",
+                         "kernel": ("md_verify_attn_full_append" if fused_step else "md_verify_attn_full")
+                         + " (attn_tc_kernel: tcgen05 MMAs with TMEM accumulators, stream-K persistent, fused split merge"
+                         + (", fused kv_append)" if fused_step else ")"),
                          "algorithmic_bytes_per_launch": vb, "ms_per_launch": round(v_ms, 4),
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
             "verify_gbs": round(v_gbs, 1),
@@ -633,6 +666,8 @@ def main(argv=None):
     ap.add_argument("--layers", type=int, default=0, help="override the model's layer count")
     ap.add_argument("--rot", type=int, default=4, help="physically distinct layer caches cycled through")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-fused-append", action="store_true",
+                    help="separate md_kv_append launches instead of the *_append attention calls")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-ar", action="store_true")

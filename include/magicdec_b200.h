@@ -196,6 +196,33 @@ MD_API md_status md_draft_attn_sparse_windows(const md_kv_cache* cache, const vo
                                               void* workspace, size_t workspace_bytes, md_stream_t stream);
 
 /*
+ * md_verify_attn_full_append / md_draft_attn_sparse_append — the append of a pass fused into
+ * its attention call (SURVEY §8(a) row a1 "can be fused into the attention prologue"; the
+ * step of §8(a): kv_append(start = L_b + j) then draft, kv_append(start = L_b) then verify).
+ * Exactly equivalent to
+ *     md_kv_append(cache, k_new, v_new, T, start = kv_len - T);  then the plain call
+ * (T = 1 for the draft call), in one kernel launch: the CTA that streams the key tile holding a
+ * new row writes that row into the cache before its TMA load of the tile (the K/V of the new
+ * rows come from k_new / v_new, so the attention reads exactly what md_kv_append would write).
+ *   k_new, v_new: device bf16 [B][T][Hkv][head_dim], contiguous, 16-byte aligned (as for
+ *                 md_kv_append); the cache rows [kv_len[b] - T, kv_len[b]) are overwritten.
+ *   All other arguments, outputs, workspace and limits: as md_verify_attn_full /
+ *   md_draft_attn_sparse.  The draft form needs window >= 1 (the new token is in its window).
+ * The fused form runs the static stream-K plan (no dynamic tail); where the kernel the shape
+ * selects cannot fuse (the mma.sync rows kernel: head_dim 64 verify with g*T > 8), the call
+ * enqueues the md_kv_append kernel ahead of the attention kernel instead — same results.
+ * Preconditions (device): as the plain calls, plus T <= kv_len[b].
+ */
+MD_API md_status md_verify_attn_full_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads, int32_t T,
+                                     const void* k_new, const void* v_new, const int32_t* kv_len,
+                                     int32_t max_kv_len, float scale, float* out, float* lse, void* workspace,
+                                     size_t workspace_bytes, md_stream_t stream);
+MD_API md_status md_draft_attn_sparse_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                      const void* k_new, const void* v_new, const int32_t* kv_len, int32_t sink,
+                                      int32_t window, float scale, float* out, float* lse, void* workspace,
+                                      size_t workspace_bytes, md_stream_t stream);
+
+/*
  * md_draft_attn_indexed — self-speculative draft attention over a static SnapKV-selected KV
  * (the paper's best drafter; SnapKV with observation
  * window 32 and average pooling 5; per-sequence budgets).

@@ -30,7 +30,8 @@ ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_works
                "md_snapkv_select", "md_philox_u32", "md_spec_accept", "md_debug_trace",
                "md_verify_attn_tree", "md_spec_accept_tree", "md_kv_compact", "md_pq_encode", "md_pq_workspace_bytes",
                "md_pq_select", "md_verify_attn_full_tp", "md_draft_attn_sparse_tp", "md_tp_barrier",
-               "md_philox_u32_dev", "md_draft_attn_sparse_windows")
+               "md_philox_u32_dev", "md_draft_attn_sparse_windows", "md_verify_attn_full_append",
+               "md_draft_attn_sparse_append")
 
 
 class MDError(RuntimeError):
@@ -84,6 +85,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                          c_void_p, sz, c_void_p]
     lib.md_draft_attn_sparse_windows.argtypes = [pc, c_void_p, i32, c_void_p, i32, i32, c_void_p, f32, c_void_p,
                                                  c_void_p, c_void_p, sz, c_void_p]
+    lib.md_verify_attn_full_append.argtypes = [pc, c_void_p, i32, i32, c_void_p, c_void_p, c_void_p, i32, f32,
+                                               c_void_p, c_void_p, c_void_p, sz, c_void_p]
+    lib.md_draft_attn_sparse_append.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, c_void_p, i32, i32, f32,
+                                                c_void_p, c_void_p, c_void_p, sz, c_void_p]
     lib.md_draft_attn_indexed.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, i32, c_void_p, c_void_p, f32,
                                           c_void_p, c_void_p, c_void_p, sz, c_void_p]
     lib.md_snapkv_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
@@ -205,6 +210,38 @@ def draft_attn_sparse(q, k_cache, v_cache, kv_len, sink, window, scale, out, lse
         return
     _check(lib.md_draft_attn_sparse(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(kv_len), int(sink), int(window),
                                     float(scale), _ptr(out), _ptr(lse), ws, wsb, _stream(stream)))
+
+
+def _need_contiguous(*ts):
+    for t in ts:
+        if not t.is_contiguous():
+            raise ValueError("k_new / v_new must be contiguous [B, T, Hkv, d]")
+
+
+def verify_attn_full_append(q, k_cache, v_cache, k_new, v_new, kv_len, max_kv_len, scale, out, lse=None,
+                            workspace=None, stream=None):
+    """kv_append(k_new, v_new at kv_len - T) fused into verify_attn_full: one kernel launch.
+    k_new / v_new [B, T, Hkv, d] bf16 contiguous."""
+    _need_contiguous(k_new, v_new)
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_verify_attn_full_append(ctypes.byref(c), _ptr(q), q.shape[2], q.shape[1], _ptr(k_new),
+                                          _ptr(v_new), _ptr(kv_len), int(max_kv_len), float(scale), _ptr(out),
+                                          _ptr(lse), ws, wsb, _stream(stream)))
+
+
+def draft_attn_sparse_append(q, k_cache, v_cache, k_new, v_new, kv_len, sink, window, scale, out, lse=None,
+                             workspace=None, stream=None):
+    """kv_append(k_new, v_new at kv_len - 1) fused into draft_attn_sparse: one kernel launch.
+    k_new / v_new [B, 1, Hkv, d] bf16 contiguous."""
+    _need_contiguous(k_new, v_new)
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_draft_attn_sparse_append(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(k_new), _ptr(v_new),
+                                           _ptr(kv_len), int(sink), int(window), float(scale), _ptr(out), _ptr(lse),
+                                           ws, wsb, _stream(stream)))
 
 
 def draft_attn_indexed(q, k_cache, v_cache, kv_len, idx, idx_count, tail_start, scale, out, lse=None,

@@ -87,6 +87,13 @@ struct AttnParams {
   int tp_world, out_hq, out_h0;
   int pdl_early;          // tcgen05 kernel: trigger the dependent launch at entry (1) or at exit (0)
   const int32_t* windows; // MODE_DRAFT: per-sequence windows [B] or nullptr (p.window for all)
+  // fused append (md_*_append): new K/V rows [B][T][Hkv][D] written to cache rows [n-T, n) by
+  // the CTA that owns their tile (append_own_rows); null for the plain calls
+  const uint16_t* kn;
+  const uint16_t* vn;
+  uint16_t* kw;                    // writable cache base pointers
+  uint16_t* vw;
+  int64_t c_sB, c_sH, c_sS;        // cache strides in elements
   int mode;
   float scale_log2;       // scale * log2(e)
 };
@@ -289,6 +296,44 @@ __device__ __forceinline__ Ranges seg_ranges(const AttnParams& p, const Seg& sg)
 }
 
 
+// ------------------------------------------------------------------ fused append (a1 in a2/a3)
+// md_draft_attn_sparse_append / md_verify_attn_full_append: the T new K/V rows of every
+// (b, kv head) go to cache rows [n-T, n) inside the attention kernel, i.e. exactly
+// md_kv_append(start = kv_len - T) followed by the attention call.  Every key tile belongs to
+// exactly one CTA's static range and every new row lies in some tile (verify reads [0, n); a
+// draft window >= 1 ends at n), so each CTA writes the new rows of its own tiles and no CTA
+// reads a row another CTA writes.  The writers order their generic stores before the async
+// proxy (fence.proxy.async.global) and arrive on an mbarrier that the producer waits on before
+// issuing a tile holding a new row (tile_has_new).  Static plans only (the host sets dyn_k = 0).
+__device__ __forceinline__ bool tile_has_new(const AttnParams& p, int n, int pos, int nvalid) {
+  return p.kn != nullptr && pos < n && pos + nvalid > n - p.T;
+}
+template <int D>
+__device__ void append_own_rows(const AttnParams& p, const int* pre, int64_t S, int64_t E, int tid, int nthr) {
+  constexpr int NV = D / 8;  // 16-byte vectors per row
+  SegWalker w;
+  w.init(p, pre, S, E);
+  Seg sg;
+  while (w.next(p, pre, sg)) {
+    const Ranges rg = seg_ranges(p, sg);
+    const int n = sg.n, nb = n - p.T;
+    const int64_t ubase = (int64_t)sg.b * p.c_sB + (int64_t)sg.kvh * p.c_sH;
+    for (int part = 0; part < 2; ++part) {
+      const int a = max(part ? rg.s1 : rg.s0, nb), e = min(part ? rg.e1 : rg.e0, n);
+      for (int i = tid; i < (e - a) * NV; i += nthr) {
+        const int r = a + i / NV, c = (i % NV) * 8;
+        const int64_t src = (((int64_t)sg.b * p.T + (r - nb)) * p.Hkv + sg.kvh) * D + c;
+        const int64_t dst = ubase + (int64_t)r * p.c_sS + c;
+        const uint4 kv = __ldg(reinterpret_cast<const uint4*>(p.kn + src));
+        const uint4 vv = __ldg(reinterpret_cast<const uint4*>(p.vn + src));
+        *reinterpret_cast<uint4*>(p.kw + dst) = kv;
+        *reinterpret_cast<uint4*>(p.vw + dst) = vv;
+      }
+    }
+  }
+  fence_proxy_async_global();
+}
+
 // diagnostics: consumer warp 0 / lane 0 stamps phase k of this CTA (md_debug_trace)
 constexpr int TRACE_SLOTS = 16;
 // Diagnostics (md_debug_trace): slot 0 entry, 1 after the grid-dependency wait, 2 range
@@ -336,7 +381,7 @@ __device__ __forceinline__ void store_out(const AttnParams& p, int64_t off, V v)
 template <int D, int NSTAGE>
 __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapSet& tm, const Ranges& rg, int b,
                                                 int kvh, uint8_t* ring, uint64_t* full, uint64_t* empty, int& it,
-                                                uint64_t pol) {
+                                                uint64_t pol, int n = 0, uint64_t* apb = nullptr) {
   constexpr int SUB = D / 64, TILE = TK * D * 2, STAGE = 2 * TILE;
   const int lane = threadIdx.x & 31;
   const bool gathered0 = (p.mode == MODE_INDEXED);
@@ -389,6 +434,7 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
         continue;
       }
       if (lane != 0) continue;
+      if (apb != nullptr && tile_has_new(p, n, pos, nvalid)) mbar_wait(apb, 0);  // fused append done
       mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
       if (nvalid == TK) {  // full tile: one TK-row box per 128-byte column slab
         mbar_arrive_expect_tx(&full[stage], STAGE);
@@ -937,7 +983,8 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   uint64_t* qempty = qfull + 2;
   uint64_t* cfull = qempty + 2;   // dynamic chunk hand-off, producer -> consumers (2 slots)
   uint64_t* cempty = cfull + 2;
-  int* cids = reinterpret_cast<int*>(cempty + 2);
+  uint64_t* apb = cempty + 2;     // fused append: the consumers' new-row stores are done
+  int* cids = reinterpret_cast<int*>(apb + 1);
   int* flag = cids + 2;  // [4] finish_unit
   Plan* plan_smem = reinterpret_cast<Plan*>(flag + 4);  // 40 bytes (reserved 48)
   int* pre = flag + 16;  // [TABLE_B + 1] per-sequence tile prefix
@@ -954,6 +1001,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       mbar_init(&cfull[s], 1);
       mbar_init(&cempty[s], NC);
     }
+    mbar_init(apb, NC);
     fence_mbar_init();
   }
   // query rows >= R of both Q slots stay zero for the whole kernel
@@ -983,6 +1031,11 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
   Seg sg;
   trace_stamp(p, 2);
+  if (p.kn != nullptr && warp < NC) {  // fused append: the new rows of this CTA's tiles
+    append_own_rows<D>(p, pre, pl.start(chunk), pl.start(chunk + 1), threadIdx.x, NC * 32);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(apb);
+  }
 
   if (warp == NC) {
     // ============================== TMA producer warp ==============================
@@ -1030,7 +1083,8 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
           bulk_load(qbuf + (qs * C::ROWS + r) * C::QSTR, p.q + out_row(p, sg.b, sg.kvh, r) * D, D * 2, &qfull[qs]);
       }
       __syncwarp();
-      produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol);
+      produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol, sg.n,
+                                 p.kn != nullptr ? apb : nullptr);
       ++qi;
     }
     if (lane == 0) trace_put(p, 10, globaltimer());
@@ -1513,6 +1567,8 @@ struct IndexedArgs {
   const uint32_t* tree_mask = nullptr;  // verify only
   const md_tp_out* tp = nullptr;        // f1: outputs stored into every TP rank's full-head buffer
   const int32_t* windows = nullptr;     // draft: per-sequence windows
+  const void* k_new = nullptr;          // fused append (md_*_append): [B][T][Hkv][d] rows for [n-T, n)
+  const void* v_new = nullptr;
 };
 
 static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int T, const int32_t* kv_len, int sink,
@@ -1552,8 +1608,26 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
     MD_REQUIRE(c->stride_s % c->head_dim == 0 && c->stride_h % c->head_dim == 0 && c->stride_b % c->head_dim == 0,
                MD_ERR_UNSUPPORTED, "%s: cache strides must be multiples of head_dim for row gathers", who);
   }
+  bool fuse_append = false;
+  if (ix.k_new != nullptr) {
+    MD_REQUIRE(ix.v_new != nullptr && aligned16(ix.k_new) && aligned16(ix.v_new), MD_ERR_INVALID_ARG,
+               "%s: k_new / v_new must be non-NULL and 16-byte aligned", who);
+    // the keys and tcgen05 kernels write the new rows themselves; the rows kernel (d = 64 verify,
+    // MD_TC=0) gets the same rows from a kv_append launch ahead of it
+    fuse_append = (tcg || use_keys_kernel(R)) && env_int("MD_FUSED_APPEND", 1) != 0;
+    if (!fuse_append && (st = launch_kv_append(c, ix.k_new, ix.v_new, T, kv_len, -T, s)) != MD_OK) return st;
+  }
   AttnParams p{};
   p.q = static_cast<const uint16_t*>(q);
+  if (fuse_append) {
+    p.kn = static_cast<const uint16_t*>(ix.k_new);
+    p.vn = static_cast<const uint16_t*>(ix.v_new);
+    p.kw = static_cast<uint16_t*>(c->k);
+    p.vw = static_cast<uint16_t*>(c->v);
+  }
+  p.c_sB = c->stride_b;
+  p.c_sH = c->stride_h;
+  p.c_sS = c->stride_s;
   p.out = out;
   p.lse = lse;
   p.kv_len = kv_len;
@@ -1585,6 +1659,7 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.row_sH = c->stride_h / c->head_dim;
   p.row_sS = c->stride_s / c->head_dim;
   p.dyn_k = tcg ? tc_dyn_k() : dyn_k_for(R);  // the tcgen05 kernel's dynamic tail (make_plan)
+  if (fuse_append) p.dyn_k = 0;  // the new rows are written per static range (append_own_rows)
   p.dyn_static_permille = dyn_static_permille();
   p.dyn_min_tiles = dyn_min_tiles();
   const size_t chunks = (size_t)grid * (1 + p.dyn_k);
@@ -1741,6 +1816,43 @@ extern "C" md_status md_draft_attn_sparse_tp(const md_kv_cache* cache, const voi
   ix.tp = tp;
   return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, nullptr, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_tp", ix);
+}
+
+extern "C" md_status md_verify_attn_full_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                                int32_t T, const void* k_new, const void* v_new,
+                                                const int32_t* kv_len, int32_t max_kv_len, float scale, float* out,
+                                                float* lse, void* workspace, size_t workspace_bytes,
+                                                md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(T >= 1 && T <= 16, MD_ERR_UNSUPPORTED, "md_verify_attn_full_append: T must be in [1, 16]");
+  MD_REQUIRE(cache != nullptr, MD_ERR_INVALID_ARG, "md_verify_attn_full_append: NULL cache");
+  MD_REQUIRE(k_new != nullptr && v_new != nullptr, MD_ERR_INVALID_ARG, "md_verify_attn_full_append: NULL k_new/v_new");
+  MD_REQUIRE(max_kv_len >= T && max_kv_len <= cache->capacity, MD_ERR_INVALID_ARG,
+             "md_verify_attn_full_append: need T <= max_kv_len <= capacity");
+  IndexedArgs ix;
+  ix.k_new = k_new;
+  ix.v_new = v_new;
+  return run_attention(cache, q, num_q_heads, T, kv_len, 0, 0, MODE_VERIFY, scale, out, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_verify_attn_full_append", ix);
+}
+
+extern "C" md_status md_draft_attn_sparse_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                                 const void* k_new, const void* v_new, const int32_t* kv_len,
+                                                 int32_t sink, int32_t window, float scale, float* out, float* lse,
+                                                 void* workspace, size_t workspace_bytes, md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(cache != nullptr, MD_ERR_INVALID_ARG, "md_draft_attn_sparse_append: NULL cache");
+  MD_REQUIRE(k_new != nullptr && v_new != nullptr, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_append: NULL k_new/v_new");
+  MD_REQUIRE(sink >= 0 && window >= 1, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_append: need sink >= 0 and window >= 1 (the draft token attends to itself)");
+  IndexedArgs ix;
+  ix.k_new = k_new;
+  ix.v_new = v_new;
+  return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, out, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_append", ix);
 }
 
 extern "C" MD_API md_status md_debug_trace(void* buf, size_t bytes) {

@@ -121,7 +121,7 @@ template <int NP>
 __device__ void produce(const AttnParams& p, const TmapSet& tm, const CUtensorMap* qmap, const Seg& sg,
                         const Ranges& rg, uint8_t* ring, uint8_t* qbuf, uint64_t* full, uint64_t* empty,
                         uint64_t* vfull, uint64_t* vempty, uint64_t* qfull, uint64_t* qempty, int& it, int& qi,
-                        PendV& pend, uint64_t pol, long long* tw) {
+                        PendV& pend, uint64_t pol, long long* tw, uint64_t* apb) {
   using C = Cfg<NP>;
   const int qs = qi % C::NQ;
   mbar_wait(&qempty[qs], ((qi / C::NQ) & 1) ^ 1);
@@ -132,6 +132,7 @@ __device__ void produce(const AttnParams& p, const TmapSet& tm, const CUtensorMa
   for (int pos = rg.s0; pos < rg.e0; pos += KT, ++it) {
     const int stage = it % C::NSTAGE;
     const int nvalid = min(KT, rg.e0 - pos);
+    if (tile_has_new(p, sg.n, pos, nvalid)) mbar_wait(apb, 0);  // fused append done
     twait(&empty[stage], ((it / C::NSTAGE) & 1) ^ 1, tw);
     mbar_arrive_expect_tx(&full[stage], half_bytes(nvalid));
     // L2 prefetch PF stages ahead (full 64-row boxes only)
@@ -179,7 +180,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* cempty = cfull + 2;      // [2]
   uint64_t* vfull = cempty + 2;      // [NSTAGE] V halves of the ring stages (full / empty: K halves)
   uint64_t* vempty = vfull + NSTAGE; // [NSTAGE]
-  int* cids = reinterpret_cast<int*>(vempty + NSTAGE);  // [2]
+  uint64_t* apb = vempty + NSTAGE;   // [1] fused append: the softmax warps' new-row stores are done
+  int* cids = reinterpret_cast<int*>(apb + 1);  // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(cids + 2);
   int* flag = reinterpret_cast<int*>(tslot + 4);                 // [16] finish_unit
   Plan* plan_smem = reinterpret_cast<Plan*>(flag + 16);          // 40 bytes (reserved 64)
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&cfull[s2], 1);
       mbar_init(&cempty[s2], 5);  // the MMA thread + one arrival per softmax warp
     }
+    mbar_init(apb, 4);
     fence_mbar_init();
   }
   // Q rows >= R stay zero for the whole kernel (the TMA boxes write rows < R only)
@@ -245,6 +248,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   SegWalker walk;
   Seg sg;
   if (active) walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+  if (p.kn != nullptr && warp < 4 && active) {  // fused append: the new rows of this CTA's tiles
+    append_own_rows<128>(p, pre, pl.start(chunk), pl.start(chunk + 1), threadIdx.x, SM_THREADS);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(apb);
+  }
 
   if (warp == 4) {
     // ============================== TMA producer ==============================
@@ -280,7 +288,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           continue;
         }
         produce<NP>(p, tm, &qmap, sg, seg_ranges(p, sg), ring, qbuf, full, empty, vfull, vempty, qfull, qempty, it, qi,
-                    pend, pol, twp);
+                    pend, pol, twp, apb);
       }
       if (pend.it >= 0) issue_v<NSTAGE>(tm, ring, vfull, vempty, pend, pol);
       if (p.trace) trace_put(p, 15, tw);

@@ -10,7 +10,8 @@ namespace md {
 __global__ void __launch_bounds__(256) kv_append_kernel(uint16_t* __restrict__ kc, uint16_t* __restrict__ vc,
                                                         const uint16_t* __restrict__ kn,
                                                         const uint16_t* __restrict__ vn,
-                                                        const int32_t* __restrict__ start, int T, int Hkv, int d,
+                                                        const int32_t* __restrict__ start, int start_off, int T,
+                                                        int Hkv, int d,
                                                         int64_t sB, int64_t sH, int64_t sS, int64_t nvec) {
   pdl_trigger();
   pdl_wait();
@@ -22,7 +23,7 @@ __global__ void __launch_bounds__(256) kv_append_kernel(uint16_t* __restrict__ k
     const int64_t bt = row / Hkv;
     const int t = static_cast<int>(bt % T);
     const int b = static_cast<int>(bt / T);
-    const int64_t dst = b * sB + h * sH + (int64_t)(__ldg(start + b) + t) * sS + c;
+    const int64_t dst = b * sB + h * sH + (int64_t)(__ldg(start + b) + start_off + t) * sS + c;
     const uint4 kv = __ldg(reinterpret_cast<const uint4*>(kn + row * d + c));
     const uint4 vv = __ldg(reinterpret_cast<const uint4*>(vn + row * d + c));
     *reinterpret_cast<uint4*>(kc + dst) = kv;
@@ -48,14 +49,24 @@ extern "C" md_status md_kv_append(const md_kv_cache* c, const void* k_new, const
              "md_kv_append: cache strides must be multiples of 8 elements");
   MD_REQUIRE(aligned16(c->k) && aligned16(c->v) && aligned16(k_new) && aligned16(v_new), MD_ERR_INVALID_ARG,
              "md_kv_append: pointers must be 16-byte aligned");
+  return launch_kv_append(c, k_new, v_new, T, start_pos, 0, (cudaStream_t)stream);
+}
+
+namespace md {
+// rows [start[b] + start_off, + T) of every (b, kv head); start_off = -T with start = kv_len is
+// the append of the fused attention calls when their kernel cannot fuse it (attn.cu)
+md_status launch_kv_append(const md_kv_cache* c, const void* k_new, const void* v_new, int T, const int32_t* start,
+                           int start_off, cudaStream_t stream) {
   const int64_t nvec = (int64_t)c->batch * T * c->num_kv_heads * (c->head_dim / 8);
   const int threads = 256;
   int64_t blocks = (nvec + threads - 1) / threads;
   const int64_t cap_blocks = (int64_t)device_sm_count() * 16;
   if (blocks > cap_blocks) blocks = cap_blocks;
-  launch_pdl(kv_append_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0, (cudaStream_t)stream,
+  launch_pdl(kv_append_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0, stream,
              static_cast<uint16_t*>(c->k), static_cast<uint16_t*>(c->v), static_cast<const uint16_t*>(k_new),
-             static_cast<const uint16_t*>(v_new), start_pos, (int)T, (int)c->num_kv_heads, (int)c->head_dim,
+             static_cast<const uint16_t*>(v_new), start, start_off, (int)T, (int)c->num_kv_heads, (int)c->head_dim,
              (int64_t)c->stride_b, (int64_t)c->stride_h, (int64_t)c->stride_s, nvec);
   return check_launch("md_kv_append");
 }
+
+}  // namespace md

@@ -34,6 +34,9 @@ inline md_status check_launch(const char* what) {
 
 int device_sm_count();
 
+md_status launch_kv_append(const md_kv_cache* c, const void* k_new, const void* v_new, int T, const int32_t* start,
+                           int start_off, cudaStream_t stream);
+
 }  // namespace md
 
 #define MD_REQUIRE(cond, code, ...)  \

@@ -69,6 +69,19 @@ def test_host_side_validation_without_gpu():
     assert st == md.MD_ERR_INVALID_ARG
     st, _ = _err(lib.md_kv_append(ctypes.byref(c), None, 16, 1, 16, None))
     assert st == md.MD_ERR_INVALID_ARG
+    # fused append calls: NULL new rows, a draft window that would not hold the new row, T range
+    st, msg = _err(lib.md_draft_attn_sparse_append(ctypes.byref(c), 16, 4, None, 16, 16, 4, 60, 0.1, 16, None, None,
+                                                   0, None))
+    assert st == md.MD_ERR_INVALID_ARG and "k_new" in msg
+    st, msg = _err(lib.md_draft_attn_sparse_append(ctypes.byref(c), 16, 4, 16, 16, 16, 4, 0, 0.1, 16, None, None,
+                                                   0, None))
+    assert st == md.MD_ERR_INVALID_ARG and "window >= 1" in msg
+    st, msg = _err(lib.md_verify_attn_full_append(ctypes.byref(c), 16, 4, 5, None, 16, 16, 64, 0.1, 16, None, None,
+                                                  0, None))
+    assert st == md.MD_ERR_INVALID_ARG and "k_new" in msg
+    st, _ = _err(lib.md_verify_attn_full_append(ctypes.byref(c), 16, 4, 17, 16, 16, 16, 64, 0.1, 16, None, None,
+                                                0, None))
+    assert st == md.MD_ERR_UNSUPPORTED
 
 
 def test_workspace_query_is_host_only():

@@ -1,0 +1,149 @@
+"""GPU parity of the fused append calls (md_verify_attn_full_append, md_draft_attn_sparse_append):
+each must equal md_kv_append(start = kv_len - T) followed by the plain call, so the oracle is
+oracle.attention.kv_append then oracle.attention.verify_attn_full / draft_attn_sparse on the
+updated cache.  Outputs within the attention tolerance, the whole cache after the
+call bit-exact.  The cache rows [n - T, n) hold other data before the call (the synth cache), so
+a tile loaded before its new rows landed shows up as an output mismatch.
+"""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2408_11049_b200 as md
+import synth as S
+from oracle import attention as OA
+from tests.helpers import AttnCase, bits_to_torch_bf16
+
+pytestmark = pytest.mark.gpu
+
+ATOL_O = 2e-3
+ATOL_LSE = 1e-3
+
+
+def _bits(t):
+    return t.cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+def _new_rows(seed, B, T, Hkv, d):
+    kn = S.k_to_bf16_bits(S.new_kv_k(seed, S.T_KNEW, B, T, Hkv, d))
+    vn = S.k_to_bf16_bits(S.new_kv_k(seed, S.T_VNEW, B, T, Hkv, d))
+    return kn, vn
+
+
+def _cmp(o, l, ro, rl):
+    assert np.all(np.isfinite(o)) and np.all(np.isfinite(l))
+    eo, el = np.max(np.abs(o - ro)), np.max(np.abs(l - rl))
+    assert eo <= ATOL_O and el <= ATOL_LSE, (eo, el)
+
+
+VERIFY_CASES = [
+    # name,            B, Hq, Hkv,  d,  T, lengths                  kernel
+    ("llama3_gqa",     3, 32, 8, 128, 5, [1500, 1497, 64]),      # tcgen05, R = 20
+    ("qwen_gqa",       2, 28, 4, 128, 5, [2100, 777]),           # tcgen05, R = 35
+    ("tc_generic_24",  2, 16, 4, 128, 6, [2000, 133]),           # tcgen05, runtime R = 24
+    ("tile_straddle",  2, 32, 8, 128, 5, [130, 66]),             # new rows across a 64/128-key tile edge
+    ("llama2_mha",     2, 32, 32, 128, 4, [1000, 517]),          # keys kernel (R = 4)
+    ("decode_T1",      2, 32, 8, 128, 1, [300, 1]),              # keys kernel, n = T
+    ("d64_rows",       4, 8, 2, 64, 3, [3, 65, 128, 129]),       # rows kernel: kv_append launch ahead
+    ("tiny",           2, 4, 4, 64, 4, [256, 256]),
+]
+
+
+@pytest.mark.parametrize("name,B,Hq,Hkv,d,T,lens", VERIFY_CASES)
+def test_verify_append_parity(name, B, Hq, Hkv, d, T, lens):
+    seed = zlib.crc32(name.encode()) & 0xFFFF
+    case = AttnCase(B, Hq, Hkv, d, max(lens) + 7, lens, T=T, seed=seed).to_cuda()
+    kn, vn = _new_rows(seed + 1, B, T, Hkv, d)
+    mkl = int(case.kv_len.max())
+    out = torch.full((B, T, Hq, d), float("nan"), device="cuda")
+    lse = torch.full((B, T, Hq), float("nan"), device="cuda")
+    ws = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, T, mkl), dtype=torch.uint8, device="cuda")
+    md.verify_attn_full_append(case.qv, case.k, case.v, bits_to_torch_bf16(kn), bits_to_torch_bf16(vn),
+                               case.kv_len_t, mkl, case.scale, out, lse, ws)
+    torch.cuda.synchronize()
+    kc, vc = case.k_bits.copy(), case.v_bits.copy()
+    OA.kv_append(kc, vc, kn, vn, case.kv_len - T)
+    ro, rl = OA.verify_attn_full(case.qv_bits, kc, vc, case.kv_len, case.scale)
+    _cmp(out.cpu().numpy(), lse.cpu().numpy(), ro, rl)
+    assert np.array_equal(_bits(case.k), kc) and np.array_equal(_bits(case.v), vc)
+
+
+DRAFT_CASES = [
+    # name,           B, Hq, Hkv, d, lengths, sink, window
+    ("llama3",        3, 32, 8, 128, [3000, 1025, 1024], 4, 1020),
+    ("qwen",          2, 28, 4, 128, [4100, 2049], 4, 2044),
+    ("llama2",        2, 32, 32, 128, [2000, 600], 4, 508),
+    ("short_seq",     3, 8, 2, 64, [1, 5, 63], 4, 60),      # new row inside the sink rows (n <= sink)
+    ("no_sink",       2, 8, 8, 64, [500, 90], 0, 77),
+    ("window_1",      2, 8, 2, 128, [700, 3], 4, 1),        # the window is the new row alone
+]
+
+
+@pytest.mark.parametrize("name,B,Hq,Hkv,d,lens,sink,window", DRAFT_CASES)
+def test_draft_append_parity(name, B, Hq, Hkv, d, lens, sink, window):
+    seed = zlib.crc32(name.encode()) & 0xFFFF
+    case = AttnCase(B, Hq, Hkv, d, max(lens) + 3, lens, seed=seed).to_cuda()
+    kn, vn = _new_rows(seed + 2, B, 1, Hkv, d)
+    out = torch.full((B, Hq, d), float("nan"), device="cuda")
+    lse = torch.full((B, Hq), float("nan"), device="cuda")
+    ws = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, 1, sink + window), dtype=torch.uint8, device="cuda")
+    md.draft_attn_sparse_append(case.qd, case.k, case.v, bits_to_torch_bf16(kn), bits_to_torch_bf16(vn),
+                                case.kv_len_t, sink, window, case.scale, out, lse, ws)
+    torch.cuda.synchronize()
+    kc, vc = case.k_bits.copy(), case.v_bits.copy()
+    OA.kv_append(kc, vc, kn, vn, case.kv_len - 1)
+    ro, rl = OA.draft_attn_sparse(case.qd_bits, kc, vc, case.kv_len, sink, window, case.scale)
+    _cmp(out.cpu().numpy(), lse.cpu().numpy(), ro, rl)
+    assert np.array_equal(_bits(case.k), kc) and np.array_equal(_bits(case.v), vc)
+
+
+def test_fused_step_sequence():
+    """One speculation step of one layer through the fused calls, back to back on one stream
+    (gamma draft calls, each appending its row, then the verify call overwriting those rows):
+    every call's output and the final cache against the oracle's kv_append + attention chain."""
+    B, Hq, Hkv, d, gamma, sink, window = 3, 32, 8, 128, 4, 4, 1020
+    T = gamma + 1
+    L = np.array([3000, 1100, 1021], dtype=np.int32)
+    case = AttnCase(B, Hq, Hkv, d, int(L.max()) + T + 3, L + T, T=T, seed=77).to_cuda()
+    kc, vc = case.k_bits.copy(), case.v_bits.copy()
+    wsd = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, 1, sink + window), dtype=torch.uint8, device="cuda")
+    wsv = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, T, int(L.max()) + T), dtype=torch.uint8, device="cuda")
+    outs, refs = [], []
+    for j in range(gamma):
+        kn, vn = _new_rows(100 + j, B, 1, Hkv, d)
+        n = (L + j + 1).astype(np.int32)
+        out = torch.empty((B, Hq, d), device="cuda")
+        lse = torch.empty((B, Hq), device="cuda")
+        md.draft_attn_sparse_append(case.qd, case.k, case.v, bits_to_torch_bf16(kn), bits_to_torch_bf16(vn),
+                                    torch.from_numpy(n).cuda(), sink, window, case.scale, out, lse, wsd)
+        outs.append((out, lse))
+        OA.kv_append(kc, vc, kn, vn, n - 1)
+        refs.append(OA.draft_attn_sparse(case.qd_bits, kc, vc, n, sink, window, case.scale))
+    kn, vn = _new_rows(200, B, T, Hkv, d)
+    n = (L + T).astype(np.int32)
+    out = torch.empty((B, T, Hq, d), device="cuda")
+    lse = torch.empty((B, T, Hq), device="cuda")
+    md.verify_attn_full_append(case.qv, case.k, case.v, bits_to_torch_bf16(kn), bits_to_torch_bf16(vn),
+                               torch.from_numpy(n).cuda(), int(n.max()), case.scale, out, lse, wsv)
+    outs.append((out, lse))
+    OA.kv_append(kc, vc, kn, vn, n - T)
+    refs.append(OA.verify_attn_full(case.qv_bits, kc, vc, n, case.scale))
+    torch.cuda.synchronize()
+    for (o, l), (ro, rl) in zip(outs, refs):
+        _cmp(o.cpu().numpy(), l.cpu().numpy(), ro, rl)
+    assert np.array_equal(_bits(case.k), kc) and np.array_equal(_bits(case.v), vc)
+
+
+def test_fused_append_rejects_bad_args():
+    case = AttnCase(2, 8, 2, 128, 300, [200, 100]).to_cuda()
+    kn = torch.zeros((2, 1, 2, 128), dtype=torch.bfloat16, device="cuda")
+    kn_wide = torch.zeros((2, 1, 2, 256), dtype=torch.bfloat16, device="cuda")  # a non-contiguous view
+    out = torch.empty((2, 8, 128), device="cuda")
+    ws = torch.zeros(md.attn_workspace_bytes(2, 8, 2, 128, 1, 64), dtype=torch.uint8, device="cuda")
+    with pytest.raises(md.MDError, match="window >= 1"):
+        md.draft_attn_sparse_append(case.qd, case.k, case.v, kn, kn, case.kv_len_t, 4, 0, case.scale, out, None, ws)
+    with pytest.raises(ValueError):
+        md.draft_attn_sparse_append(case.qd, case.k, case.v, kn_wide[..., :128], kn, case.kv_len_t, 4, 60,
+                                    case.scale, out, None, ws)
