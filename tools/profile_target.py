@@ -1,6 +1,7 @@
 """Run a few md_verify_attn_full / md_draft_attn_sparse calls of one bench config (for ncu).
 
-usage: python tools/profile_target.py [config] [n_calls]"""
+usage: python tools/profile_target.py [config] [n_calls] [fused]
+("fused": the md_*_append calls, with the new K/V rows written inside the kernel, as bench.py runs them)"""
 import os
 import sys
 
@@ -15,6 +16,7 @@ from bench import CONFIGS, SEED  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "llama3_b64_32k"
 ncalls = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+fused = len(sys.argv) > 3 and sys.argv[3] == "fused"
 B, Hq, Hkv, d, ctx, gamma, sink, window, V, layers, alpha = CONFIGS[cfg]
 T, R = gamma + 1, 2
 cap = ctx + 64
@@ -42,9 +44,17 @@ out_d = torch.empty((B, Hq, d), device="cuda")
 lse_d = torch.empty((B, Hq), device="cuda")
 ws_v = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, T, mkl)), dtype=torch.uint8, device="cuda")
 ws_d = torch.zeros(max(1, md.attn_workspace_bytes(B, Hq, Hkv, d, 1, sink + window)), dtype=torch.uint8, device="cuda")
+knv = torch.zeros((B, T, Hkv, d), dtype=torch.bfloat16, device="cuda")
+knd = torch.zeros((B, 1, Hkv, d), dtype=torch.bfloat16, device="cuda")
 for i in range(ncalls):
-    md.verify_attn_full(qv, kc[i % R], vc[i % R], kvv, mkl, scale, out_v, lse_v, ws_v)
+    if fused:
+        md.verify_attn_full_append(qv, kc[i % R], vc[i % R], knv, knv, kvv, mkl, scale, out_v, lse_v, ws_v)
+    else:
+        md.verify_attn_full(qv, kc[i % R], vc[i % R], kvv, mkl, scale, out_v, lse_v, ws_v)
 for i in range(ncalls):
-    md.draft_attn_sparse(qd, kc[i % R], vc[i % R], kvd, sink, window, scale, out_d, lse_d, ws_d)
+    if fused:
+        md.draft_attn_sparse_append(qd, kc[i % R], vc[i % R], knd, knd, kvd, sink, window, scale, out_d, lse_d, ws_d)
+    else:
+        md.draft_attn_sparse(qd, kc[i % R], vc[i % R], kvd, sink, window, scale, out_d, lse_d, ws_d)
 torch.cuda.synchronize()
 print("profile_target done", cfg)
