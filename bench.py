@@ -240,37 +240,44 @@ def run_gpu(args):
         for j in range(gamma):
             for l in range(layers):
                 kb, vb = kc[l % R], vc[l % R]
-                if fused and xd is None and world == 1:  # append fused into the draft call (one launch)
-                    md.draft_attn_sparse_append(qd, kb, vb, knew_d, vnew_d, pos[j + 1], sink, window, scale, out_d,
-                                                lse_d, ws_d)
-                    continue
-                md.kv_append(kb, vb, knew_d, vnew_d, pos[j])
+                # fused: the append runs inside the draft kernel (one launch per layer-call)
+                kn_, vn_ = (knew_d, vnew_d) if fused else (None, None)
+                if not fused:
+                    md.kv_append(kb, vb, knew_d, vnew_d, pos[j])
                 if xd is not None:
-                    md.draft_attn_sparse_tp(qd, kb, vb, pos[j + 1], sink, window, scale, xd.out, lse_d, ws_d)
+                    md.draft_attn_sparse_tp(qd, kb, vb, pos[j + 1], sink, window, scale, xd.out, lse_d, ws_d,
+                                            k_new=kn_, v_new=vn_)
                     xd.barrier()
                     continue
-                md.draft_attn_sparse(qd, kb, vb, pos[j + 1], sink, window, scale, out_d, lse_d, ws_d)
+                if fused:
+                    md.draft_attn_sparse_append(qd, kb, vb, knew_d, vnew_d, pos[j + 1], sink, window, scale, out_d,
+                                                lse_d, ws_d)
+                else:
+                    md.draft_attn_sparse(qd, kb, vb, pos[j + 1], sink, window, scale, out_d, lse_d, ws_d)
                 if world > 1:
                     gather_rank_major(out_d, gath_d)
         for l in range(layers):
             kb, vb = kc[l % R], vc[l % R]
-            if fused and xv is None and world == 1:  # append fused into the verify call (one launch)
-                md.verify_attn_full_append(qv, kb, vb, knew_v, vnew_v, pos[gamma + 1], max_kv, scale, out_v, lse_v,
-                                           ws_v)
-                continue
-            md.kv_append(kb, vb, knew_v, vnew_v, pos[0])
+            kn_, vn_ = (knew_v, vnew_v) if fused else (None, None)
+            if not fused:
+                md.kv_append(kb, vb, knew_v, vnew_v, pos[0])
             if xv is not None:
-                md.verify_attn_full_tp(qv, kb, vb, pos[gamma + 1], max_kv, scale, xv.out, lse_v, ws_v)
+                md.verify_attn_full_tp(qv, kb, vb, pos[gamma + 1], max_kv, scale, xv.out, lse_v, ws_v,
+                                       k_new=kn_, v_new=vn_)
                 xv.barrier()
                 continue
-            md.verify_attn_full(qv, kb, vb, pos[gamma + 1], max_kv, scale, out_v, lse_v, ws_v)
+            if fused:
+                md.verify_attn_full_append(qv, kb, vb, knew_v, vnew_v, pos[gamma + 1], max_kv, scale, out_v, lse_v,
+                                           ws_v)
+            else:
+                md.verify_attn_full(qv, kb, vb, pos[gamma + 1], max_kv, scale, out_v, lse_v, ws_v)
             if world > 1:
                 gather_rank_major(out_v, gath_v)
 
     # per layer-call: md_kv_append + one attention kernel (stream-K, merge fused); + philox + accept
     launches_per_step = gamma * layers * 2 + layers * 2 + 2
-    if fused and world == 1:
-        launches_per_step = gamma * layers + layers + 2
+    if fused:
+        launches_per_step -= gamma * layers + layers
     if world > 1:
         launches_per_step += gamma * layers + layers  # the exchange after every attention call
 
@@ -374,7 +381,7 @@ def run_gpu(args):
 
     # the kernels the step runs: with the fused append, the *_append calls (their algorithmic
     # bytes add the new rows read from k_new / v_new and written to the cache: 4 B*T*Hkv*d*2)
-    fused_step = fused and world == 1
+    fused_step = fused
     if fused_step:
         v_ms = time_calls(lambda r: md.verify_attn_full_append(qv, kc[r % R], vc[r % R], knew_v, vnew_v, kv_len_v,
                                                                max_kv, scale, out_v, lse_v, ws_v))
@@ -467,7 +474,7 @@ def run_gpu(args):
                 if c < gamma * layers:
                     j = c // layers
                     q_, k_, v_ = st_d[sl]
-                    if fused and world == 1:
+                    if fused:
                         md.draft_attn_sparse_append(q_, kb, vb_, k_, v_, pos_buf[j + 1], sink, window, scale, out_d,
                                                     lse_d, ws_d)
                     else:
@@ -477,7 +484,7 @@ def run_gpu(args):
                         gather_rank_major(out_d, gath_d)
                 else:
                     q_, k_, v_ = st_v[sl]
-                    if fused and world == 1:
+                    if fused:
                         md.verify_attn_full_append(q_, kb, vb_, k_, v_, pos_buf[gamma + 1], max_kv, scale, out_v,
                                                    lse_v, ws_v)
                     else:
@@ -541,7 +548,7 @@ def run_gpu(args):
                        "attention_only": True,
                        "cuda_graph": ("layer loop" if split else "whole step (drafts + verify + philox + accept)")
                        if use_graph else False,
-                       "kv_append": "fused into the attention calls" if fused and world == 1 else "separate launches",
+                       "kv_append": "fused into the attention calls" if fused else "separate launches",
                        "parallelism": (f"tp{world} (KV heads, {exchange} exchange)" if world > 1
                                        else "single GPU")},
             "tokens_per_step": round(tokens / args.steps, 3),

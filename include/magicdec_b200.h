@@ -359,6 +359,19 @@ MD_API md_status md_draft_attn_sparse_tp(const md_kv_cache* cache, const void* q
                                          const int32_t* kv_len, int32_t sink, int32_t window, float scale,
                                          const md_tp_out* tp, float* lse, void* workspace, size_t workspace_bytes,
                                          md_stream_t stream);
+/*
+ * md_verify_attn_full_tp_append / md_draft_attn_sparse_tp_append — the _tp calls with the
+ * rank's append fused in, exactly as md_verify_attn_full_append / md_draft_attn_sparse_append
+ * (k_new, v_new: this rank's KV heads, [B][T][Hkv_local][head_dim]); outputs as the _tp calls.
+ */
+MD_API md_status md_verify_attn_full_tp_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                        int32_t T, const void* k_new, const void* v_new, const int32_t* kv_len,
+                                        int32_t max_kv_len, float scale, const md_tp_out* tp, float* lse,
+                                        void* workspace, size_t workspace_bytes, md_stream_t stream);
+MD_API md_status md_draft_attn_sparse_tp_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                         const void* k_new, const void* v_new, const int32_t* kv_len, int32_t sink,
+                                         int32_t window, float scale, const md_tp_out* tp, float* lse,
+                                         void* workspace, size_t workspace_bytes, md_stream_t stream);
 
 /*
  * md_tp_barrier — completion barrier of the fused exchange: every rank calls it once after each

@@ -31,7 +31,7 @@ ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_works
                "md_verify_attn_tree", "md_spec_accept_tree", "md_kv_compact", "md_pq_encode", "md_pq_workspace_bytes",
                "md_pq_select", "md_verify_attn_full_tp", "md_draft_attn_sparse_tp", "md_tp_barrier",
                "md_philox_u32_dev", "md_draft_attn_sparse_windows", "md_verify_attn_full_append",
-               "md_draft_attn_sparse_append")
+               "md_draft_attn_sparse_append", "md_verify_attn_full_tp_append", "md_draft_attn_sparse_tp_append")
 
 
 class MDError(RuntimeError):
@@ -109,6 +109,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                            c_void_p]
     lib.md_draft_attn_sparse_tp.argtypes = [pc, c_void_p, i32, c_void_p, i32, i32, f32, ptp, c_void_p, c_void_p, sz,
                                             c_void_p]
+    lib.md_verify_attn_full_tp_append.argtypes = [pc, c_void_p, i32, i32, c_void_p, c_void_p, c_void_p, i32, f32,
+                                                  ptp, c_void_p, c_void_p, sz, c_void_p]
+    lib.md_draft_attn_sparse_tp_append.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, c_void_p, i32, i32, f32,
+                                                   ptp, c_void_p, c_void_p, sz, c_void_p]
     lib.md_tp_barrier.argtypes = [psync, c_void_p]
     lib.md_philox_u32_dev.argtypes = [u64, c_void_p, i32, i32, c_void_p, c_void_p]
     lib.md_pq_encode.argtypes = [pc, c_void_p, c_void_p, i32, c_void_p, i32, c_void_p]
@@ -314,21 +318,37 @@ def tp_sync(flags_peers_dev, epoch_dev, world, rank) -> TPSync:
     return TPSync(_ptr(flags_peers_dev), _ptr(epoch_dev), int(world), int(rank))
 
 
-def verify_attn_full_tp(q, k_cache, v_cache, kv_len, max_kv_len, scale, tp, lse=None, workspace=None, stream=None):
-    """Rank-local verify whose outputs land in every rank's [B, T, world*Hq, d] buffer (tp: TPOut)."""
+def verify_attn_full_tp(q, k_cache, v_cache, kv_len, max_kv_len, scale, tp, lse=None, workspace=None, stream=None,
+                        k_new=None, v_new=None):
+    """Rank-local verify whose outputs land in every rank's [B, T, world*Hq, d] buffer (tp: TPOut).
+    With k_new / v_new ([B, T, Hkv_local, d]) the rank's append is fused in (md_verify_attn_full_tp_append)."""
     lib = load_library()
     c = make_cache(k_cache, v_cache)
     ws, wsb = _ws(workspace)
+    if k_new is not None:
+        _need_contiguous(k_new, v_new)
+        _check(lib.md_verify_attn_full_tp_append(ctypes.byref(c), _ptr(q), q.shape[2], q.shape[1], _ptr(k_new),
+                                                 _ptr(v_new), _ptr(kv_len), int(max_kv_len), float(scale),
+                                                 ctypes.byref(tp), _ptr(lse), ws, wsb, _stream(stream)))
+        return
     _check(lib.md_verify_attn_full_tp(ctypes.byref(c), _ptr(q), q.shape[2], q.shape[1], _ptr(kv_len),
                                       int(max_kv_len), float(scale), ctypes.byref(tp), _ptr(lse), ws, wsb,
                                       _stream(stream)))
 
 
-def draft_attn_sparse_tp(q, k_cache, v_cache, kv_len, sink, window, scale, tp, lse=None, workspace=None, stream=None):
-    """Rank-local StreamingLLM draft whose outputs land in every rank's [B, world*Hq, d] buffer."""
+def draft_attn_sparse_tp(q, k_cache, v_cache, kv_len, sink, window, scale, tp, lse=None, workspace=None, stream=None,
+                         k_new=None, v_new=None):
+    """Rank-local StreamingLLM draft whose outputs land in every rank's [B, world*Hq, d] buffer.
+    With k_new / v_new ([B, 1, Hkv_local, d]) the rank's append is fused in (md_draft_attn_sparse_tp_append)."""
     lib = load_library()
     c = make_cache(k_cache, v_cache)
     ws, wsb = _ws(workspace)
+    if k_new is not None:
+        _need_contiguous(k_new, v_new)
+        _check(lib.md_draft_attn_sparse_tp_append(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(k_new), _ptr(v_new),
+                                                  _ptr(kv_len), int(sink), int(window), float(scale),
+                                                  ctypes.byref(tp), _ptr(lse), ws, wsb, _stream(stream)))
+        return
     _check(lib.md_draft_attn_sparse_tp(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(kv_len), int(sink), int(window),
                                        float(scale), ctypes.byref(tp), _ptr(lse), ws, wsb, _stream(stream)))
 

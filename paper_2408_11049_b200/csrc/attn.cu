@@ -1855,6 +1855,47 @@ extern "C" md_status md_draft_attn_sparse_append(const md_kv_cache* cache, const
                        workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_append", ix);
 }
 
+extern "C" md_status md_verify_attn_full_tp_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                                   int32_t T, const void* k_new, const void* v_new,
+                                                   const int32_t* kv_len, int32_t max_kv_len, float scale,
+                                                   const md_tp_out* tp, float* lse, void* workspace,
+                                                   size_t workspace_bytes, md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(T >= 1 && T <= 16, MD_ERR_UNSUPPORTED, "md_verify_attn_full_tp_append: T must be in [1, 16]");
+  MD_REQUIRE(cache != nullptr && tp != nullptr, MD_ERR_INVALID_ARG, "md_verify_attn_full_tp_append: NULL cache / tp");
+  MD_REQUIRE(k_new != nullptr && v_new != nullptr, MD_ERR_INVALID_ARG,
+             "md_verify_attn_full_tp_append: NULL k_new/v_new");
+  MD_REQUIRE(max_kv_len >= T && max_kv_len <= cache->capacity, MD_ERR_INVALID_ARG,
+             "md_verify_attn_full_tp_append: need T <= max_kv_len <= capacity");
+  IndexedArgs ix;
+  ix.tp = tp;
+  ix.k_new = k_new;
+  ix.v_new = v_new;
+  return run_attention(cache, q, num_q_heads, T, kv_len, 0, 0, MODE_VERIFY, scale, nullptr, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_verify_attn_full_tp_append", ix);
+}
+
+extern "C" md_status md_draft_attn_sparse_tp_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                                    const void* k_new, const void* v_new, const int32_t* kv_len,
+                                                    int32_t sink, int32_t window, float scale, const md_tp_out* tp,
+                                                    float* lse, void* workspace, size_t workspace_bytes,
+                                                    md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(cache != nullptr && tp != nullptr, MD_ERR_INVALID_ARG, "md_draft_attn_sparse_tp_append: NULL cache / tp");
+  MD_REQUIRE(k_new != nullptr && v_new != nullptr, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_tp_append: NULL k_new/v_new");
+  MD_REQUIRE(sink >= 0 && window >= 1, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_tp_append: need sink >= 0 and window >= 1 (the draft token attends to itself)");
+  IndexedArgs ix;
+  ix.tp = tp;
+  ix.k_new = k_new;
+  ix.v_new = v_new;
+  return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, nullptr, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_tp_append", ix);
+}
+
 extern "C" MD_API md_status md_debug_trace(void* buf, size_t bytes) {
   md::g_trace = static_cast<unsigned long long*>(buf);
   md::g_trace_bytes = bytes;

@@ -142,4 +142,10 @@ def test_host_side_validation_of_selection_and_tp_calls():
     assert st == md.MD_ERR_WORKSPACE
     st, msg = _err(lib.md_pq_encode(ctypes.byref(_cache(d=96)), 16, 16, 10, 16, 100, None))
     assert st == md.MD_ERR_UNSUPPORTED
+    st, msg = _err(lib.md_verify_attn_full_tp_append(ctypes.byref(c), 16, 4, 5, None, 16, 16, 64, 0.1, None, None,
+                                                     None, 0, None))
+    assert st == md.MD_ERR_INVALID_ARG
+    st, msg = _err(lib.md_draft_attn_sparse_tp_append(ctypes.byref(c), 16, 4, 16, 16, 16, 4, 0, 0.1, None, None,
+                                                      None, 0, None))
+    assert st == md.MD_ERR_INVALID_ARG
     assert md.pq_workspace_bytes(2, 2, 1000) > 0 and md.pq_workspace_bytes(0, 2, 1000) == 0

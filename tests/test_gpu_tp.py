@@ -92,6 +92,60 @@ def test_fused_tp_verify_and_draft(world):
             assert rv.flags[r].cpu().tolist() == [it + 1] * world
 
 
+def test_fused_tp_append_verify_and_draft():
+    """The _tp_append calls: each rank appends its own KV heads' new rows inside its attention
+    kernel and stores its heads into every rank's buffer; against the oracle's kv_append +
+    unsharded attention (verify appends T rows at kv_len - T, then the draft one row at kv_len - 1)."""
+    world, B, Hq, Hkv, d, T = 2, 3, 32, 8, 128, 5
+    lens = [2500, 1700, 300]
+    case = AttnCase(B, Hq, Hkv, d, max(lens) + 8, lens, T=T, seed=17)
+    kvl = torch.from_numpy(case.kv_len).cuda()
+    kn = S.k_to_bf16_bits(S.new_kv_k(5, S.T_KNEW, B, T, Hkv, d))
+    vn = S.k_to_bf16_bits(S.new_kv_k(5, S.T_VNEW, B, T, Hkv, d))
+    knd = S.k_to_bf16_bits(S.new_kv_k(6, S.T_KNEW, B, 1, Hkv, d))
+    vnd = S.k_to_bf16_bits(S.new_kv_k(6, S.T_VNEW, B, 1, Hkv, d))
+    kc, vc = case.k_bits.copy(), case.v_bits.copy()
+    OA.kv_append(kc, vc, kn, vn, case.kv_len - T)
+    ref_v, _ = OA.verify_attn_full(case.qv_bits, kc, vc, case.kv_len, case.scale)
+    OA.kv_append(kc, vc, knd, vnd, case.kv_len - 1)
+    ref_d, _ = OA.draft_attn_sparse(case.qd_bits, kc, vc, case.kv_len, 4, 252, case.scale)
+    rv, rd = Ranks(world, (B, T, Hq, d)), Ranks(world, (B, Hq, d))
+    shards = [_shard(case, world, r) for r in range(world)]
+    qper, kvper = Hq // world, Hkv // world
+    part = lambda a, r: bits_to_torch_bf16(np.ascontiguousarray(a[:, :, r * kvper:(r + 1) * kvper]))
+    news = [(part(kn, r), part(vn, r), part(knd, r), part(vnd, r)) for r in range(world)]
+    ws = [torch.zeros(md.attn_workspace_bytes(B, qper, kvper, d, T, max(lens)), dtype=torch.uint8, device="cuda")
+          for _ in range(world)]
+    wsd = [torch.zeros(md.attn_workspace_bytes(B, qper, kvper, d, 1, 256), dtype=torch.uint8, device="cuda")
+           for _ in range(world)]
+    outs_v, outs_d = [rv.out(r) for r in range(world)], [rd.out(r) for r in range(world)]
+    syncs_v, syncs_d = [rv.sync(r) for r in range(world)], [rd.sync(r) for r in range(world)]
+    # warm-up of both kernel variants on scratch copies (shared-memory attributes; see above)
+    k, v, qv, qd, _, _ = shards[0]
+    k0, v0 = k.clone(), v.clone()
+    md.verify_attn_full_append(qv, k0, v0, news[0][0], news[0][1], kvl, max(lens), case.scale,
+                               torch.empty_like(rv.bufs[0][:, :, :qper]), None, ws[0])
+    md.draft_attn_sparse_append(qd, k0, v0, news[0][2], news[0][3], kvl, 4, 252, case.scale,
+                                torch.empty_like(rd.bufs[0][:, :qper]), None, wsd[0])
+    torch.cuda.synchronize()
+    for r in range(world):
+        k, v, qv, qd, _, _ = shards[r]
+        s = rv.streams[r]
+        md.verify_attn_full_tp(qv, k, v, kvl, max(lens), case.scale, outs_v[r], None, ws[r], stream=s,
+                               k_new=news[r][0], v_new=news[r][1])
+        md.tp_barrier(syncs_v[r], stream=s)
+        md.draft_attn_sparse_tp(qd, k, v, kvl, 4, 252, case.scale, outs_d[r], None, wsd[r], stream=s,
+                                k_new=news[r][2], v_new=news[r][3])
+        md.tp_barrier(syncs_d[r], stream=s)
+    torch.cuda.synchronize()
+    for r in range(world):
+        assert np.max(np.abs(rv.bufs[r].cpu().numpy() - ref_v)) <= ATOL_O
+        assert np.max(np.abs(rd.bufs[r].cpu().numpy() - ref_d)) <= ATOL_O
+        k, v = shards[r][0], shards[r][1]
+        got = k.cpu().view(torch.int16).numpy().view(np.uint16)
+        assert np.array_equal(got, kc[:, r * kvper:(r + 1) * kvper])
+
+
 def test_tp_world1_equals_plain_call():
     """world = 1: the _tp call writes exactly what the plain call writes (bit for bit)."""
     case = AttnCase(2, 32, 8, 128, 1100, [1000, 777], T=5, seed=95).to_cuda()
