@@ -443,15 +443,23 @@ def run_gpu(args):
         nd = gamma * layers                      # draft calls come first, then the verify calls
         bounds = [[(n * c) // layers for c in range(layers + 1)] for n in (x[0].numel() for x in flat_pq)]
 
+        # graph mode (world == 1): the whole e2e step -- H2D copies on the copy stream, the calls,
+        # uniforms, acceptance and the D2H read-back -- is captured once and replayed per step;
+        # replays on one stream are serialised, so only waits on events recorded in the same
+        # capture are kept (`recorded`)
+        recorded = None
+
         def issue_copy(c):
             sl = c % NB
             with torch.cuda.stream(copy_s):
-                copy_s.wait_event(done[sl])
+                if recorded is None or ("done", sl) in recorded:
+                    copy_s.wait_event(done[sl])
                 dst, src = (st_d[sl], (h_qd, h_kd, h_vd)) if c < gamma * layers else (st_v[sl], (h_qv, h_kv, h_vv))
                 for x, y in zip(dst, src):
                     x.copy_(y, non_blocking=True)
                 if c == nd:
-                    copy_s.wait_event(acc_done)  # the previous step's acceptance has read p / q
+                    if recorded is None:
+                        copy_s.wait_event(acc_done)  # the previous step's acceptance has read p / q
                     dtok.copy_(h_d, non_blocking=True)
                 if c >= nd:
                     v = c - nd
@@ -463,6 +471,10 @@ def run_gpu(args):
 
         def e2e_step(i):
             cur = torch.cuda.current_stream()
+            if recorded is not None:  # fork the copy stream from the capturing stream
+                fork = torch.cuda.Event()
+                fork.record(cur)
+                copy_s.wait_event(fork)
             for c0 in range(min(NB - 1, ncalls)):
                 issue_copy(c0)
             torch.add(committed[None, :], ar, out=pos_buf)
@@ -493,10 +505,16 @@ def run_gpu(args):
                     if world > 1:
                         gather_rank_major(out_v, gath_v)
                 done[sl].record(cur)
+                if recorded is not None:
+                    recorded.add(("done", sl))
                 if c + NB - 1 < ncalls:
                     issue_copy(c + NB - 1)
             cur.wait_event(pq_ready)
-            md.philox_u32(SEED, i, rnd)
+            if recorded is not None:
+                md.philox_u32_dev(SEED, step_dev, rnd)  # the step counter lives in device memory
+                step_dev.add_(1)
+            else:
+                md.philox_u32(SEED, i, rnd)
             md.spec_accept(p_t, q_t, dtok, rnd, out_tok, nacc, committed, mode="sample")
             acc_done.record(cur)
             h_out.copy_(out_tok, non_blocking=True)
@@ -504,12 +522,31 @@ def run_gpu(args):
 
         e2e_step(10_000)
         torch.cuda.synchronize()
+        g_e2e = None
+        if world == 1 and not args.no_graph:
+            try:
+                recorded = set()
+                g_e2e = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g_e2e):
+                    e2e_step(0)
+                torch.cuda.synchronize()
+            except Exception as e:  # noqa: BLE001 - the eager loop below is the same step
+                print(f"e2e graph capture failed ({type(e).__name__}: {e}); timing the eager loop", file=sys.stderr)
+                g_e2e = None
+                torch.cuda.synchronize()
+            recorded = None
+            if g_e2e is not None:
+                g_e2e.replay()  # warm-up replay
+                torch.cuda.synchronize()
         k_e2e = max(1, min(args.steps, 5))
         c1 = committed.clone()
         a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         for i in range(k_e2e):
-            e2e_step(20_000 + i)
+            if g_e2e is not None:
+                g_e2e.replay()
+            else:
+                e2e_step(20_000 + i)
         b_.record()
         torch.cuda.synchronize()
         e_ms = a.elapsed_time(b_)
@@ -519,7 +556,8 @@ def run_gpu(args):
             e_ms = float(t.item())
         e_tok = int((committed - c1).sum().item())
         e2e = {"value": round(e_tok / (e_ms / 1e3), 2), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "steps": k_e2e}
+               "d2h_bytes_per_step": int(d2h), "steps": k_e2e,
+               "cuda_graph": ("whole step incl. H2D / D2H copies" if g_e2e is not None else False)}
 
     result = None
     if rank == 0:
