@@ -1569,6 +1569,7 @@ struct IndexedArgs {
   const int32_t* windows = nullptr;     // draft: per-sequence windows
   const void* k_new = nullptr;          // fused append (md_*_append): [B][T][Hkv][d] rows for [n-T, n)
   const void* v_new = nullptr;
+  int max_keys = 0;                     // fused append: upper bound of the keys per unit (plan choice)
 };
 
 static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int T, const int32_t* kv_len, int sink,
@@ -1615,6 +1616,11 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
     // the keys and tcgen05 kernels write the new rows themselves; the rows kernel (d = 64 verify,
     // MD_TC=0) gets the same rows from a kv_append launch ahead of it
     fuse_append = (tcg || use_keys_kernel(R)) && env_int("MD_FUSED_APPEND", 1) != 0;
+    // a long keys-kernel call (the MHA verify) runs the dynamic tail (make_plan), which the fused
+    // append cannot serve (its rows are written per static range): keep the tail and enqueue the
+    // append kernel ahead instead (decided on an upper bound of the tile count)
+    const int64_t tiles_ub = (int64_t)c->batch * c->num_kv_heads * ((ix.max_keys + TK - 1) / TK);
+    if (fuse_append && !tcg && dyn_k_for(R) > 0 && tiles_ub >= (int64_t)dyn_min_tiles() * grid) fuse_append = false;
     if (!fuse_append && (st = launch_kv_append(c, ix.k_new, ix.v_new, T, kv_len, -T, s)) != MD_OK) return st;
   }
   AttnParams p{};
@@ -1833,6 +1839,7 @@ extern "C" md_status md_verify_attn_full_append(const md_kv_cache* cache, const 
   IndexedArgs ix;
   ix.k_new = k_new;
   ix.v_new = v_new;
+  ix.max_keys = max_kv_len;
   return run_attention(cache, q, num_q_heads, T, kv_len, 0, 0, MODE_VERIFY, scale, out, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_verify_attn_full_append", ix);
 }
@@ -1851,6 +1858,7 @@ extern "C" md_status md_draft_attn_sparse_append(const md_kv_cache* cache, const
   IndexedArgs ix;
   ix.k_new = k_new;
   ix.v_new = v_new;
+  ix.max_keys = (int)std::min<int64_t>((int64_t)sink + window, cache->capacity);
   return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, out, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_append", ix);
 }
@@ -1872,6 +1880,7 @@ extern "C" md_status md_verify_attn_full_tp_append(const md_kv_cache* cache, con
   ix.tp = tp;
   ix.k_new = k_new;
   ix.v_new = v_new;
+  ix.max_keys = max_kv_len;
   return run_attention(cache, q, num_q_heads, T, kv_len, 0, 0, MODE_VERIFY, scale, nullptr, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_verify_attn_full_tp_append", ix);
 }
@@ -1892,6 +1901,7 @@ extern "C" md_status md_draft_attn_sparse_tp_append(const md_kv_cache* cache, co
   ix.tp = tp;
   ix.k_new = k_new;
   ix.v_new = v_new;
+  ix.max_keys = (int)std::min<int64_t>((int64_t)sink + window, cache->capacity);
   return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, nullptr, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_tp_append", ix);
 }

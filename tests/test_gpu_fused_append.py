@@ -47,6 +47,7 @@ VERIFY_CASES = [
     ("llama2_mha",     2, 32, 32, 128, 4, [1000, 517]),          # keys kernel (R = 4)
     ("decode_T1",      2, 32, 8, 128, 1, [300, 1]),              # keys kernel, n = T
     ("d64_rows",       4, 8, 2, 64, 3, [3, 65, 128, 129]),       # rows kernel: kv_append launch ahead
+    ("mha_long",       4, 32, 32, 128, 4, [19000, 18000, 19005, 300]),  # keys kernel, long: append launch ahead
     ("tiny",           2, 4, 4, 64, 4, [256, 256]),
 ]
 
