@@ -209,8 +209,10 @@ MD_API md_status md_draft_attn_sparse_windows(const md_kv_cache* cache, const vo
  *   All other arguments, outputs, workspace and limits: as md_verify_attn_full /
  *   md_draft_attn_sparse.  The draft form needs window >= 1 (the new token is in its window).
  * The fused form runs the static stream-K plan (no dynamic tail); where the kernel the shape
- * selects cannot fuse (the mma.sync rows kernel: head_dim 64 verify with g*T > 8), the call
- * enqueues the md_kv_append kernel ahead of the attention kernel instead — same results.
+ * selects cannot fuse (the mma.sync rows kernel: head_dim 64 verify with g*T > 8) or a long
+ * keys-kernel call would use the dynamic tail (B * Hkv * ceil(max_kv_len / 64) >= 128 tiles per
+ * CTA, e.g. the MHA verify), the call enqueues the md_kv_append kernel ahead of the attention
+ * kernel instead — same results.
  * Preconditions (device): as the plain calls, plus T <= kv_len[b].
  */
 MD_API md_status md_verify_attn_full_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads, int32_t T,
