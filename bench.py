@@ -425,67 +425,59 @@ def run_gpu(args):
                layers * (h_qv.nbytes + h_kv.nbytes + h_vv.nbytes) + h_p.nbytes + h_q.nbytes + h_d.nbytes)
         d2h = h_out.nbytes + h_n.nbytes
 
-        # Copies run on their own stream into NB staging slots per call kind, so the H2D traffic
-        # of call c+NB-1 overlaps the kernels of call c (a serving loop would prefetch the same way).
+        # Every call has its own device staging slot (223 MB at the target point), and all of a
+        # step's H2D copies are issued up front on their own stream, in call order; the compute
+        # stream waits only at a few group boundaries (calls [0,1), [1,8), [8,32), then every 32),
+        # so the copy engine runs ahead (55 GB/s vs ~15 GB/s of inputs consumed by the draft calls)
+        # while consecutive kernels keep their programmatic-dependent-launch overlap (an event
+        # wait before every call cost ~4 us per call).  p / q (295 MB) ride behind the verify
+        # inputs and are waited for only by the acceptance.
         copy_s = torch.cuda.Stream()
-        NB = 4  # staging slots: a call's inputs are copied NB - 1 calls ahead of it
-        st_d = [(torch.empty_like(qd), torch.empty_like(knew_d), torch.empty_like(vnew_d)) for _ in range(NB)]
-        st_v = [(torch.empty_like(qv), torch.empty_like(knew_v), torch.empty_like(vnew_v)) for _ in range(NB)]
-        ready = [torch.cuda.Event() for _ in range(NB)]
-        done = [torch.cuda.Event() for _ in range(NB)]
-        pq_ready, acc_done = torch.cuda.Event(), torch.cuda.Event()
         ncalls = gamma * layers + layers
-
-        # p / q (295 MB at the target point) are copied in slices riding along with the inputs of
-        # the verify calls (long enough to hide them), so no call's inputs queue behind one large
-        # copy and the short draft calls never wait for the copy engine
-        flat_pq = [(t.view(-1), h.view(-1)) for t, h in ((p_t, h_p), (q_t, h_q))]
         nd = gamma * layers                      # draft calls come first, then the verify calls
-        bounds = [[(n * c) // layers for c in range(layers + 1)] for n in (x[0].numel() for x in flat_pq)]
+        st = [(torch.empty_like(qd), torch.empty_like(knew_d), torch.empty_like(vnew_d)) if c < nd else
+              (torch.empty_like(qv), torch.empty_like(knew_v), torch.empty_like(vnew_v)) for c in range(ncalls)]
+        bounds_c = sorted({0, 1, 8, 32} | set(range(32, ncalls, 32)) | {ncalls})
+        bounds_c = [b for b in bounds_c if b <= ncalls]
+        group_of = {}
+        for gi in range(len(bounds_c) - 1):
+            for c in range(bounds_c[gi], bounds_c[gi + 1]):
+                group_of[c] = gi
+        ready = [torch.cuda.Event() for _ in range(len(bounds_c) - 1)]
+        pq_ready, step_done = torch.cuda.Event(), torch.cuda.Event()
+        in_graph = False
 
-        # graph mode (world == 1): the whole e2e step -- H2D copies on the copy stream, the calls,
-        # uniforms, acceptance and the D2H read-back -- is captured once and replayed per step;
-        # replays on one stream are serialised, so only waits on events recorded in the same
-        # capture are kept (`recorded`)
-        recorded = None
-
-        def issue_copy(c):
-            sl = c % NB
+        def issue_copies(cur):
             with torch.cuda.stream(copy_s):
-                if recorded is None or ("done", sl) in recorded:
-                    copy_s.wait_event(done[sl])
-                dst, src = (st_d[sl], (h_qd, h_kd, h_vd)) if c < gamma * layers else (st_v[sl], (h_qv, h_kv, h_vv))
-                for x, y in zip(dst, src):
-                    x.copy_(y, non_blocking=True)
-                if c == nd:
-                    if recorded is None:
-                        copy_s.wait_event(acc_done)  # the previous step's acceptance has read p / q
-                    dtok.copy_(h_d, non_blocking=True)
-                if c >= nd:
-                    v = c - nd
-                    for (t, h), bd in zip(flat_pq, bounds):
-                        t[bd[v]:bd[v + 1]].copy_(h[bd[v]:bd[v + 1]], non_blocking=True)
-                ready[sl].record(copy_s)
-                if c == ncalls - 1:
-                    pq_ready.record(copy_s)
+                if in_graph:  # fork the copy stream from the capturing stream
+                    fork = torch.cuda.Event()
+                    fork.record(cur)
+                    copy_s.wait_event(fork)
+                else:  # eager: the previous step's calls and acceptance are done with the slots / p, q
+                    copy_s.wait_event(step_done)
+                for c in range(ncalls):
+                    src = (h_qd, h_kd, h_vd) if c < nd else (h_qv, h_kv, h_vv)
+                    for x, y in zip(st[c], src):
+                        x.copy_(y, non_blocking=True)
+                    if c + 1 in bounds_c:
+                        ready[group_of[c]].record(copy_s)
+                dtok.copy_(h_d, non_blocking=True)
+                p_t.copy_(h_p, non_blocking=True)
+                q_t.copy_(h_q, non_blocking=True)
+                pq_ready.record(copy_s)
 
         def e2e_step(i):
             cur = torch.cuda.current_stream()
-            if recorded is not None:  # fork the copy stream from the capturing stream
-                fork = torch.cuda.Event()
-                fork.record(cur)
-                copy_s.wait_event(fork)
-            for c0 in range(min(NB - 1, ncalls)):
-                issue_copy(c0)
+            issue_copies(cur)
             torch.add(committed[None, :], ar, out=pos_buf)
             for c in range(ncalls):
-                sl = c % NB
-                cur.wait_event(ready[sl])
+                if c in bounds_c:
+                    cur.wait_event(ready[group_of[c]])
                 l = c % layers
                 kb, vb_ = kc[l % R], vc[l % R]
-                if c < gamma * layers:
+                q_, k_, v_ = st[c]
+                if c < nd:
                     j = c // layers
-                    q_, k_, v_ = st_d[sl]
                     if fused:
                         md.draft_attn_sparse_append(q_, kb, vb_, k_, v_, pos_buf[j + 1], sink, window, scale, out_d,
                                                     lse_d, ws_d)
@@ -495,7 +487,6 @@ def run_gpu(args):
                     if world > 1:
                         gather_rank_major(out_d, gath_d)
                 else:
-                    q_, k_, v_ = st_v[sl]
                     if fused:
                         md.verify_attn_full_append(q_, kb, vb_, k_, v_, pos_buf[gamma + 1], max_kv, scale, out_v,
                                                    lse_v, ws_v)
@@ -504,28 +495,25 @@ def run_gpu(args):
                         md.verify_attn_full(q_, kb, vb_, pos_buf[gamma + 1], max_kv, scale, out_v, lse_v, ws_v)
                     if world > 1:
                         gather_rank_major(out_v, gath_v)
-                done[sl].record(cur)
-                if recorded is not None:
-                    recorded.add(("done", sl))
-                if c + NB - 1 < ncalls:
-                    issue_copy(c + NB - 1)
             cur.wait_event(pq_ready)
-            if recorded is not None:
+            if in_graph:
                 md.philox_u32_dev(SEED, step_dev, rnd)  # the step counter lives in device memory
                 step_dev.add_(1)
             else:
                 md.philox_u32(SEED, i, rnd)
             md.spec_accept(p_t, q_t, dtok, rnd, out_tok, nacc, committed, mode="sample")
-            acc_done.record(cur)
             h_out.copy_(out_tok, non_blocking=True)
             h_n.copy_(nacc, non_blocking=True)
+            if not in_graph:
+                step_done.record(cur)
 
+        step_done.record(torch.cuda.current_stream())
         e2e_step(10_000)
         torch.cuda.synchronize()
         g_e2e = None
         if world == 1 and not args.no_graph:
             try:
-                recorded = set()
+                in_graph = True
                 g_e2e = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g_e2e):
                     e2e_step(0)
@@ -534,11 +522,14 @@ def run_gpu(args):
                 print(f"e2e graph capture failed ({type(e).__name__}: {e}); timing the eager loop", file=sys.stderr)
                 g_e2e = None
                 torch.cuda.synchronize()
-            recorded = None
+            in_graph = False
             if g_e2e is not None:
                 g_e2e.replay()  # warm-up replay
                 torch.cuda.synchronize()
-        k_e2e = max(1, min(args.steps, 5))
+        # the timed steps draw the same uniforms as the device-timed steps (Philox steps
+        # warmup .. warmup + steps - 1), so both see the same acceptances and tokens per step
+        step_dev.fill_(args.warmup)
+        k_e2e = max(1, args.steps)
         c1 = committed.clone()
         a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -546,7 +537,7 @@ def run_gpu(args):
             if g_e2e is not None:
                 g_e2e.replay()
             else:
-                e2e_step(20_000 + i)
+                e2e_step(args.warmup + i)
         b_.record()
         torch.cuda.synchronize()
         e_ms = a.elapsed_time(b_)
@@ -556,7 +547,8 @@ def run_gpu(args):
             e_ms = float(t.item())
         e_tok = int((committed - c1).sum().item())
         e2e = {"value": round(e_tok / (e_ms / 1e3), 2), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "steps": k_e2e,
+               "d2h_bytes_per_step": int(d2h), "steps": k_e2e, "ms_per_step": round(e_ms / k_e2e, 4),
+               "tokens_per_step": round(e_tok / k_e2e, 1),
                "cuda_graph": ("whole step incl. H2D / D2H copies" if g_e2e is not None else False)}
 
     result = None
