@@ -1,6 +1,7 @@
 """Where does the spec step's time go?  Captures sub-sequences of bench.py's layer pass as
 CUDA graphs and times each replay (CUDA events): verify calls alone, verify + their
-kv_append, draft calls alone, draft + kv_append, appends alone, and the whole pass.
+kv_append, draft calls alone, draft + kv_append, appends alone, the whole pass, and the same
+with the appends fused into the attention calls (md_*_append).
 usage: python tools/step_probe.py [config]"""
 import json
 import os
@@ -69,6 +70,16 @@ def appends():
         md.kv_append(kc[l % R], vc[l % R], knew_v, vnew_v, pos[0])
 
 
+def verify_fused(l):
+    md.verify_attn_full_append(qv, kc[l % R], vc[l % R], knew_v, vnew_v, pos[gamma + 1], mkl, scale, out_v, lse_v,
+                               ws_v)
+
+
+def draft_fused(j, l):
+    md.draft_attn_sparse_append(qd, kc[l % R], vc[l % R], knew_d, vnew_d, pos[j + 1], sink, window, scale, out_d,
+                                lse_d, ws_d)
+
+
 variants = {
     "verify_only": lambda: [verify(l, False) for l in range(layers)],
     "verify_append": lambda: [verify(l, True) for l in range(layers)],
@@ -77,9 +88,20 @@ variants = {
     "appends_only": appends,
     "full_pass": lambda: ([draft(j, l, True) for j in range(gamma) for l in range(layers)],
                           [verify(l, True) for l in range(layers)]),
+    "verify_fused": lambda: [verify_fused(l) for l in range(layers)],
+    "draft_fused": lambda: [draft_fused(j, l) for j in range(gamma) for l in range(layers)],
+    "full_pass_fused": lambda: ([draft_fused(j, l) for j in range(gamma) for l in range(layers)],
+                                [verify_fused(l) for l in range(layers)]),
 }
+# PROBE_VARIANTS=a,b PROBE_ROUNDS=k: only those variants, interleaved k times (A/B without drift)
+sel = os.environ.get("PROBE_VARIANTS")
+rounds = int(os.environ.get("PROBE_ROUNDS", "1"))
+order = [n for _ in range(rounds) for n in (sel.split(",") if sel else variants)]
 res = {"cfg": cfg}
-for name, fn in variants.items():
+for k, name in enumerate(order):
+    fn = variants[name]
+    if rounds > 1:
+        name = f"{name}#{k // (len(order) // rounds)}"
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
