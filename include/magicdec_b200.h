@@ -247,6 +247,21 @@ MD_API md_status md_draft_attn_indexed(const md_kv_cache* cache, const void* q, 
                                        float* lse, void* workspace, size_t workspace_bytes, md_stream_t stream);
 
 /*
+ * md_draft_attn_indexed_append — md_draft_attn_indexed with the draft step's append fused in:
+ * exactly md_kv_append(k_new, v_new, T = 1, start = kv_len - 1) followed by
+ * md_draft_attn_indexed, in one launch (the new row is streamed with the tail, so the CTA whose
+ * tail tile holds it writes it; see md_draft_attn_sparse_append).
+ *   k_new, v_new: device bf16 [B][1][Hkv][head_dim], contiguous, 16-byte aligned.
+ * Preconditions (device): as md_draft_attn_indexed, plus tail_start[b] <= kv_len[b] - 1 (the new
+ * row lies in the always-attended tail).
+ */
+MD_API md_status md_draft_attn_indexed_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                       const void* k_new, const void* v_new, const int32_t* kv_len,
+                                       const int32_t* idx, int32_t idx_stride, const int32_t* idx_count,
+                                       const int32_t* tail_start, float scale, float* out, float* lse,
+                                       void* workspace, size_t workspace_bytes, md_stream_t stream);
+
+/*
  * md_snapkv_select — SnapKV static KV selection at prefill for md_draft_attn_indexed
  * (P:1141 footnote: observation window 32, average pooling kernel 5;
  * a static method, so drafting pays no per-step selection cost, Eq.3).  Per

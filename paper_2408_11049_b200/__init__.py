@@ -31,7 +31,8 @@ ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_works
                "md_verify_attn_tree", "md_spec_accept_tree", "md_kv_compact", "md_pq_encode", "md_pq_workspace_bytes",
                "md_pq_select", "md_verify_attn_full_tp", "md_draft_attn_sparse_tp", "md_tp_barrier",
                "md_philox_u32_dev", "md_draft_attn_sparse_windows", "md_verify_attn_full_append",
-               "md_draft_attn_sparse_append", "md_verify_attn_full_tp_append", "md_draft_attn_sparse_tp_append")
+               "md_draft_attn_sparse_append", "md_verify_attn_full_tp_append", "md_draft_attn_sparse_tp_append",
+               "md_draft_attn_indexed_append")
 
 
 class MDError(RuntimeError):
@@ -89,6 +90,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                                c_void_p, c_void_p, c_void_p, sz, c_void_p]
     lib.md_draft_attn_sparse_append.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, c_void_p, i32, i32, f32,
                                                 c_void_p, c_void_p, c_void_p, sz, c_void_p]
+    lib.md_draft_attn_indexed_append.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, c_void_p, c_void_p, i32,
+                                                 c_void_p, c_void_p, f32, c_void_p, c_void_p, c_void_p, sz, c_void_p]
     lib.md_draft_attn_indexed.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, i32, c_void_p, c_void_p, f32,
                                           c_void_p, c_void_p, c_void_p, sz, c_void_p]
     lib.md_snapkv_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
@@ -249,12 +252,20 @@ def draft_attn_sparse_append(q, k_cache, v_cache, k_new, v_new, kv_len, sink, wi
 
 
 def draft_attn_indexed(q, k_cache, v_cache, kv_len, idx, idx_count, tail_start, scale, out, lse=None,
-                       workspace=None, stream=None):
+                       workspace=None, stream=None, k_new=None, v_new=None):
     """SnapKV draft: q [B, Hq, d] over idx[b, u, :idx_count[b]] U [tail_start[b], kv_len[b]).
-    idx is int32 [B, Hkv, K] (K % 4 == 0)."""
+    idx is int32 [B, Hkv, K] (K % 4 == 0).  With k_new / v_new ([B, 1, Hkv, d]) the step's append
+    at kv_len - 1 is fused in (md_draft_attn_indexed_append)."""
     lib = load_library()
     c = make_cache(k_cache, v_cache)
     ws, wsb = _ws(workspace)
+    if k_new is not None:
+        _need_contiguous(k_new, v_new)
+        _check(lib.md_draft_attn_indexed_append(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(k_new), _ptr(v_new),
+                                                _ptr(kv_len), _ptr(idx), idx.shape[2], _ptr(idx_count),
+                                                _ptr(tail_start), float(scale), _ptr(out), _ptr(lse), ws, wsb,
+                                                _stream(stream)))
+        return
     _check(lib.md_draft_attn_indexed(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(kv_len), _ptr(idx), idx.shape[2],
                                      _ptr(idx_count), _ptr(tail_start), float(scale), _ptr(out), _ptr(lse), ws, wsb,
                                      _stream(stream)))

@@ -318,7 +318,7 @@ __device__ void append_own_rows(const AttnParams& p, const int* pre, int64_t S, 
     const Ranges rg = seg_ranges(p, sg);
     const int n = sg.n, nb = n - p.T;
     const int64_t ubase = (int64_t)sg.b * p.c_sB + (int64_t)sg.kvh * p.c_sH;
-    for (int part = 0; part < 2; ++part) {
+    for (int part = p.mode == MODE_INDEXED ? 1 : 0; part < 2; ++part) {  // indexed part 0: list positions
       const int a = max(part ? rg.s1 : rg.s0, nb), e = min(part ? rg.e1 : rg.e0, n);
       for (int i = tid; i < (e - a) * NV; i += nthr) {
         const int r = a + i / NV, c = (i % NV) * 8;
@@ -1904,6 +1904,31 @@ extern "C" md_status md_draft_attn_sparse_tp_append(const md_kv_cache* cache, co
   ix.max_keys = (int)std::min<int64_t>((int64_t)sink + window, cache->capacity);
   return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, nullptr, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_tp_append", ix);
+}
+
+extern "C" md_status md_draft_attn_indexed_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                                  const void* k_new, const void* v_new, const int32_t* kv_len,
+                                                  const int32_t* idx, int32_t idx_stride, const int32_t* idx_count,
+                                                  const int32_t* tail_start, float scale, float* out, float* lse,
+                                                  void* workspace, size_t workspace_bytes, md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(cache != nullptr, MD_ERR_INVALID_ARG, "md_draft_attn_indexed_append: NULL cache");
+  MD_REQUIRE(k_new != nullptr && v_new != nullptr, MD_ERR_INVALID_ARG,
+             "md_draft_attn_indexed_append: NULL k_new/v_new");
+  MD_REQUIRE(idx != nullptr && idx_count != nullptr && tail_start != nullptr, MD_ERR_INVALID_ARG,
+             "md_draft_attn_indexed_append: NULL idx / idx_count / tail_start");
+  MD_REQUIRE(idx_stride >= 0 && idx_stride % 4 == 0 && aligned16(idx), MD_ERR_INVALID_ARG,
+             "md_draft_attn_indexed_append: idx must be 16-byte aligned with idx_stride a multiple of 4");
+  IndexedArgs ix;
+  ix.idx = idx;
+  ix.idx_stride = idx_stride;
+  ix.idx_count = idx_count;
+  ix.tail_start = tail_start;
+  ix.k_new = k_new;
+  ix.v_new = v_new;
+  return run_attention(cache, q, num_q_heads, 1, kv_len, 0, 0, MODE_INDEXED, scale, out, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_draft_attn_indexed_append", ix);
 }
 
 extern "C" MD_API md_status md_debug_trace(void* buf, size_t bytes) {

@@ -142,6 +142,9 @@ def test_host_side_validation_of_selection_and_tp_calls():
     assert st == md.MD_ERR_WORKSPACE
     st, msg = _err(lib.md_pq_encode(ctypes.byref(_cache(d=96)), 16, 16, 10, 16, 100, None))
     assert st == md.MD_ERR_UNSUPPORTED
+    st, msg = _err(lib.md_draft_attn_indexed_append(ctypes.byref(c), 16, 4, None, 16, 16, 16, 4, 16, 16, 0.1, 16,
+                                                    None, None, 0, None))
+    assert st == md.MD_ERR_INVALID_ARG and "k_new" in msg
     st, msg = _err(lib.md_verify_attn_full_tp_append(ctypes.byref(c), 16, 4, 5, None, 16, 16, 64, 0.1, None, None,
                                                      None, 0, None))
     assert st == md.MD_ERR_INVALID_ARG

@@ -194,3 +194,35 @@ def test_fused_calls_in_a_cuda_graph():
     torch.cuda.synchronize()
     for a, b in zip(ref, outs + [outv, case.k, case.v]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,lens,counts,stride,win", [
+    (3, 32, 8, 128, [3000, 2000, 700], [500, 130, 0], 512, 32),
+    (2, 28, 4, 128, [5000, 4100], [2017, 2017], 2020, 32),
+    (4, 8, 8, 64, [300, 200, 150, 90], [61, 64, 65, 3], 68, 7),
+    (2, 4, 1, 128, [9000, 40], [1000, 8], 1000, 1),           # the tail is the new row alone
+])
+def test_indexed_draft_append_parity(B, Hq, Hkv, d, lens, counts, stride, win):
+    """md_draft_attn_indexed_append (SnapKV drafting, f2) = kv_append(kv_len - 1) + the indexed draft."""
+    from oracle import snapkv as SK
+    rng = np.random.default_rng(sum(lens) + 1)
+    case = AttnCase(B, Hq, Hkv, d, max(lens) + 8, lens, seed=B * 11 + Hq).to_cuda()
+    tails = (np.asarray(lens) - win).astype(np.int32)
+    counts = np.minimum(np.asarray(counts), tails).astype(np.int32)
+    idx = np.full((B, Hkv, stride), -1, np.int32)
+    for b in range(B):
+        for h in range(Hkv):
+            idx[b, h, :counts[b]] = np.sort(rng.choice(int(tails[b]), size=int(counts[b]), replace=False))
+    kn, vn = _new_rows(B + 9, B, 1, Hkv, d)
+    out = torch.full((B, Hq, d), float("nan"), device="cuda")
+    lse = torch.full((B, Hq), float("nan"), device="cuda")
+    ws = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, 1, case.cap), dtype=torch.uint8, device="cuda")
+    md.draft_attn_indexed(case.qd, case.k, case.v, case.kv_len_t, torch.from_numpy(idx).cuda(),
+                          torch.from_numpy(counts).cuda(), torch.from_numpy(tails).cuda(), case.scale, out, lse, ws,
+                          k_new=bits_to_torch_bf16(kn), v_new=bits_to_torch_bf16(vn))
+    torch.cuda.synchronize()
+    kc, vc = case.k_bits.copy(), case.v_bits.copy()
+    OA.kv_append(kc, vc, kn, vn, case.kv_len - 1)
+    ro, rl = SK.draft_attn_indexed(case.qd_bits, kc, vc, case.kv_len, idx, counts, tails, case.scale)
+    _cmp(out.cpu().numpy(), lse.cpu().numpy(), ro, rl)
+    assert np.array_equal(_bits(case.k), kc) and np.array_equal(_bits(case.v), vc)
