@@ -37,8 +37,9 @@
  *   - Return value: MD_OK, or an error code with a message from md_last_error().
  *     Host-side argument errors are detected before anything is enqueued.  Violating a
  *     device-side precondition (values inside device arrays) is undefined behaviour.
- *   - Thread safety: calls are reentrant; the only library state is the thread-local
- *     error string.
+ *   - Thread safety: calls are reentrant; the only library state is thread-local (the error
+ *     string and the md_debug_trace diagnostics buffer).  The library reads no environment
+ *     variables: every plan choice is a compile-time constant or a function of the arguments.
  */
 #ifndef MAGICDEC_B200_H
 #define MAGICDEC_B200_H
@@ -63,7 +64,7 @@ typedef struct CUstream_st* md_stream_t; /* identical to cudaStream_t */
 typedef enum {
   MD_OK = 0,
   MD_ERR_INVALID_ARG = 1, /* bad scalar, NULL or misaligned pointer, bad stride      */
-  MD_ERR_UNSUPPORTED = 2, /* valid but not built: head_dim not in {64,128}, g*T > 64  */
+  MD_ERR_UNSUPPORTED = 2, /* valid but not built: head_dim not in {64,128}, g*T > 128 */
   MD_ERR_WORKSPACE = 3,   /* workspace NULL or smaller than md_attn_workspace_bytes   */
   MD_ERR_CUDA = 4         /* a CUDA runtime/driver call or kernel launch failed       */
 } md_status;
@@ -249,11 +250,12 @@ MD_API md_status md_draft_attn_indexed(const md_kv_cache* cache, const void* q, 
 /*
  * md_draft_attn_indexed_append — md_draft_attn_indexed with the draft step's append fused in:
  * exactly md_kv_append(k_new, v_new, T = 1, start = kv_len - 1) followed by
- * md_draft_attn_indexed, in one launch (the new row is streamed with the tail, so the CTA whose
- * tail tile holds it writes it; see md_draft_attn_sparse_append).
+ * md_draft_attn_indexed, in one launch.  When the new row lies in the streamed tail, the CTA whose
+ * tail tile holds it writes it before loading the tile (see md_draft_attn_sparse_append); when it
+ * lies before the tail (tail_start[b] = kv_len[b], e.g. after md_pq_select with window 0), the CTA
+ * holding the unit's first tile writes it and any listed copy of it reads k_new / v_new directly.
  *   k_new, v_new: device bf16 [B][1][Hkv][head_dim], contiguous, 16-byte aligned.
- * Preconditions (device): as md_draft_attn_indexed, plus tail_start[b] <= kv_len[b] - 1 (the new
- * row lies in the always-attended tail).
+ * Preconditions (device): as md_draft_attn_indexed.
  */
 MD_API md_status md_draft_attn_indexed_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
                                        const void* k_new, const void* v_new, const int32_t* kv_len,
@@ -499,8 +501,9 @@ MD_API md_status md_kv_compact(const md_kv_cache* cache, const int32_t* base, co
  * 1 after the grid-dependency wait, 2 after locating its stream-K range, 3 first K/V tile
  * landed, 4 last segment epilogue start, 5 end, 6 = the SM id, 7/8/9 last epilogue after the
  * cross-warp combine / after its stores / after the split merge, 10 producer done,
- * 11 = segments processed (slots 7-11: draft/keys kernel only).  Process-wide, not
- * thread-safe; NULL disables.
+ * 11 = segments processed (slots 7-11: draft/keys kernel only).  The setting belongs to the
+ * calling thread (thread-local, like the error string): only attention calls made from that
+ * thread stamp into `buf`.  NULL disables.
  */
 MD_API md_status md_debug_trace(void* buf, size_t bytes);
 

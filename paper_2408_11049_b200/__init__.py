@@ -165,12 +165,13 @@ def abi_version() -> int:
 
 
 def kv_append(k_cache, v_cache, k_new, v_new, start_pos, stream=None):
-    """cache[b, h, start_pos[b] + t] = new[b, t, h] for K and V; new is [B, T, Hkv, d]."""
+    """cache[b, h, start_pos[b] + t] = new[b, t, h] for K and V; new is [B, T, Hkv, d] contiguous
+    (no temporary copies: the kernel reads the caller's tensors asynchronously on `stream`)."""
+    _need_contiguous(k_new, v_new)
     lib = load_library()
     c = make_cache(k_cache, v_cache)
     T = k_new.shape[1]
-    _check(lib.md_kv_append(ctypes.byref(c), _ptr(k_new.contiguous()), _ptr(v_new.contiguous()), T,
-                            _ptr(start_pos), _stream(stream)))
+    _check(lib.md_kv_append(ctypes.byref(c), _ptr(k_new), _ptr(v_new), T, _ptr(start_pos), _stream(stream)))
 
 
 def attn_workspace_bytes(batch, num_q_heads, num_kv_heads, head_dim, T, max_kv_len) -> int:

@@ -36,13 +36,26 @@ def _nvcc(sources, out, extra=(), log=None, force=False):
         glob.glob(os.path.join(os.path.dirname(sources[0]), "*.h")) + [os.path.join(ROOT, "include", "magicdec_b200.h")]
     if not force and not _stale(out, deps):
         return False
-    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-o", out + ".tmp", *sources]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    # one nvcc per translation unit, in parallel, then one link (the units share no device code)
+    from concurrent.futures import ThreadPoolExecutor
+    objs = [out + "." + os.path.splitext(os.path.basename(s))[0] + ".o" for s in sources]
+    compile_flags = [f for f in FLAGS if f not in ("-shared", "-cudart", "static")]
+    cmds = [[NVCC, *ARCH, *compile_flags, *extra, "-c", "-o", o, s] for s, o in zip(sources, objs)]
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
+    link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fPIC", "-o", out + ".tmp", *objs]
+    if all(r.returncode == 0 for r in results):
+        results.append(subprocess.run(link, capture_output=True, text=True))
     if log is not None:
         with open(log, "w") as f:
-            f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+            for c, r in zip(cmds + [link], results):
+                f.write(" ".join(c) + "\n" + r.stdout + r.stderr)
+    for o in objs:
+        if os.path.exists(o):
+            os.remove(o)
+    bad = [r for r in results if r.returncode != 0]
+    if bad:
+        sys.stderr.write("".join(r.stdout + r.stderr for r in bad))
         raise RuntimeError(f"nvcc failed building {out}")
     os.replace(out + ".tmp", out)
     return True

@@ -1,5 +1,4 @@
 // abi.cu — library-wide ABI entry points: version, thread-local error string, device query.
-#include <cstdlib>
 
 #include "md_internal.h"
 
@@ -18,13 +17,6 @@ void set_error(const char* fmt, ...) {
 
 void clear_error() { g_last_error.clear(); }
 
-bool pdl_enabled() {
-  static const bool v = [] {
-    const char* e = getenv("MD_PDL");
-    return !(e && atoi(e) == 0);
-  }();
-  return v;
-}
 
 int device_sm_count() {
   int dev = 0, n = 0;

@@ -73,7 +73,6 @@ struct AttnParams {
   const uint16_t* kc;              // cache K / V base pointers (listed-row copies of MODE_INDEXED)
   const uint16_t* vc;
   unsigned long long* trace;       // diagnostics: [G][8] globaltimer stamps (md_debug_trace), or null
-  int fused_merge;        // 1: the last CTA of a split unit merges (acq_rel counter); 0: attn_merge_kernel
   int* dyn;               // [2] dynamic chunk counter and finished-CTA counter (zero between calls)
   float* ws_x;            // rows kernel: per-CTA [XS_FRAGS][16][D] fragment scratch (key-slice sum)
   int dyn_k;              // dynamic chunks per active CTA (0: static stream-K only)
@@ -318,8 +317,19 @@ __device__ void append_own_rows(const AttnParams& p, const int* pre, int64_t S, 
     const Ranges rg = seg_ranges(p, sg);
     const int n = sg.n, nb = n - p.T;
     const int64_t ubase = (int64_t)sg.b * p.c_sB + (int64_t)sg.kvh * p.c_sH;
-    for (int part = p.mode == MODE_INDEXED ? 1 : 0; part < 2; ++part) {  // indexed part 0: list positions
-      const int a = max(part ? rg.s1 : rg.s0, nb), e = min(part ? rg.e1 : rg.e0, n);
+    // indexed part 0 holds list positions, not rows; part 2 (indexed only): new rows before the
+    // streamed tail (tail_start > n - T, e.g. a PQ selection with window 0), which no tile
+    // streams, are written by the CTA holding the unit's first tile (listed copies of such rows
+    // read k_new / v_new directly in produce_segment, never the cache)
+    for (int part = p.mode == MODE_INDEXED ? 1 : 0; part < (p.mode == MODE_INDEXED ? 3 : 2); ++part) {
+      int a, e;
+      if (part < 2) {
+        a = max(part ? rg.s1 : rg.s0, nb);
+        e = min(part ? rg.e1 : rg.e0, n);
+      } else {
+        a = nb;
+        e = sg.lo == 0 ? min(n, __ldg(p.tail_start + sg.b)) : nb;
+      }
       for (int i = tid; i < (e - a) * NV; i += nthr) {
         const int r = a + i / NV, c = (i % NV) * 8;
         const int64_t src = (((int64_t)sg.b * p.T + (r - nb)) * p.Hkv + sg.kvh) * D + c;
@@ -421,6 +431,11 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
           const int64_t off = (ubase + (int64_t)row[u] * p.row_sS) * D;
           const uint16_t* ks = p.kc + off;
           const uint16_t* vs = p.vc + off;
+          if (p.kn != nullptr && row[u] >= n - p.T) {  // fused append: a new row, from k_new / v_new
+            const int64_t src = (((int64_t)b * p.T + (row[u] - (n - p.T))) * p.Hkv + kvh) * D;
+            ks = p.kn + src;
+            vs = p.vn + src;
+          }
 #pragma unroll
           for (int c = 0; c < D / 8; ++c) {
             const uint32_t dst = (uint32_t)((c >> 3) * TK * 128 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
@@ -505,54 +520,6 @@ __device__ void finish_unit(const AttnParams& p, const Seg& sg, const Plan& pl, 
     const float inv = W > 0.f ? 1.f / W : 0.f;
     store_out(p, o_row(p, sg.b, sg.kvh, r) * D + c4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
     if (c4 == 0 && p.lse != nullptr) p.lse[out_row(p, sg.b, sg.kvh, r)] = (W > 0.f) ? (M + __log2f(W)) * LN2 : -INFINITY;
-  }
-}
-
-// Separate split merge (fused_merge == 0): one CTA per unit, launched right after the
-// attention kernel with programmatic dependent launch; units held whole by one CTA exit.
-template <int D>
-__global__ void __launch_bounds__(128) attn_merge_kernel(const AttnParams p, int grid_attn) {
-  __shared__ int pre[TABLE_B + 1];
-  pdl_trigger();
-  pdl_wait();  // the attention kernel's partials
-  build_prefix(p, pre);
-  const int64_t total = total_tiles(p, pre);
-  if (total == 0) return;
-  const Plan pl = make_plan(p, total, grid_attn);
-  const int unit = blockIdx.x, b = unit / p.Hkv, kvh = unit - b * p.Hkv;
-  int64_t bstart = 0;
-  if (p.B <= TABLE_B) {
-    bstart = pre[b];
-  } else {
-    for (int bb = 0; bb < b; ++bb) bstart += (int64_t)unit_tiles(p, bb) * p.Hkv;
-  }
-  const int tiles = tiles_of(p, pre, b);
-  if (tiles == 0) return;
-  const int64_t ustart = bstart + (int64_t)kvh * tiles;
-  const int cf = pl.chunk_of(ustart), cl = pl.chunk_of(ustart + tiles - 1);
-  if (cf == cl) return;  // written whole by one chunk
-  constexpr int V4 = D / 4;
-  for (int idx = threadIdx.x; idx < p.R * V4; idx += blockDim.x) {
-    const int r = idx / V4, c4 = (idx - r * V4) * 4;
-    float M = -INFINITY;
-    for (int c = cf; c <= cl; ++c) M = fmaxf(M, p.ws_lse[((int64_t)c * 2 + pl.slot(ustart, c)) * p.R + r]);
-    float W = 0.f;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c = cf; c <= cl; ++c) {
-      const int64_t prow = ((int64_t)c * 2 + pl.slot(ustart, c)) * p.R + r;
-      const float ls = p.ws_lse[prow];
-      if (ls == -INFINITY) continue;
-      const float w = ex2(ls - M);
-      W += w;
-      const float4 v = *reinterpret_cast<const float4*>(p.ws_o + prow * D + c4);
-      acc.x += w * v.x;
-      acc.y += w * v.y;
-      acc.z += w * v.z;
-      acc.w += w * v.w;
-    }
-    const float inv = W > 0.f ? 1.f / W : 0.f;
-    store_out(p, o_row(p, b, kvh, r) * D + c4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
-    if (c4 == 0 && p.lse != nullptr) p.lse[out_row(p, b, kvh, r)] = (W > 0.f) ? (M + __log2f(W)) * LN2 : -INFINITY;
   }
 }
 
@@ -921,7 +888,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
         }
       }
     }
-    if (!complete && p.fused_merge) finish_unit<D>(p, sg, pl, NC * 32, flag);
+    if (!complete) finish_unit<D>(p, sg, pl, NC * 32, flag);
     named_bar_sync(1, NC * 32);  // mlbuf / lsebuf / scratch reused by the next segment
     trace_stamp(p, 5);
   }
@@ -1336,7 +1303,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       }
     }
     trace_stamp(p, 8);
-    if (!complete && p.fused_merge) finish_unit<D>(p, sg, pl, NC * 32, flag);
+    if (!complete) finish_unit<D>(p, sg, pl, NC * 32, flag);
     trace_stamp(p, 9);
     named_bar_sync(1, NC * 32);  // the epilogue buffers are reused by the next segment
     trace_stamp(p, 5);
@@ -1357,75 +1324,32 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
 
 // ------------------------------------------------------------------------------ host side
 constexpr int ROWS_CTAS_PER_SM = 2;
+constexpr int KEYS_CTAS_PER_SM = 2;  // keys kernel: 2 CTAs / SM (1 CTA with a deeper ring measured slower)
 
 static bool use_keys_kernel(int R) { return R <= 8; }
 
-// tcgen05 verify kernel for 8 < R <= 48 at head_dim 128 (MD_TC=0: the mma.sync rows kernel)
-static bool use_tc_kernel(int R, int D, int mode) {
-  static const int on = [] {
-    const char* e = getenv("MD_TC");
-    return (e && atoi(e) == 0) ? 0 : 1;
-  }();
-  return on && D == 128 && mode == 0 /*MODE_VERIFY*/ && R > 8 && R <= 48;
-}
-
-// keys kernel residency: 1 CTA / SM with a deep ring, or 2 CTAs / SM with 2 stages each
-// (tuning knob MD_KEYS_CTAS=1|2 for experiments; default 2)
-static int keys_ctas_per_sm() {
-  static const int v = [] {
-    const char* e = getenv("MD_KEYS_CTAS");
-    return (e && atoi(e) == 1) ? 1 : 2;
-  }();
-  return v;
-}
-
-// split merge: fused in the attention kernel (default) or a PDL-launched kernel (MD_MERGE=kernel)
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-
-static int fused_merge_enabled() {
-  static const int v = [] {
-    const char* e = getenv("MD_MERGE");
-    return (e && std::string(e) == "kernel") ? 0 : 1;
-  }();
-  return v;
-}
+// tcgen05 verify kernel for every R = g*T > 8 at head_dim 128 (the mma.sync rows kernel serves
+// head_dim 64 with R > 8)
+static bool use_tc_kernel(int R, int D, int mode) { return D == 128 && mode == 0 /*MODE_VERIFY*/ && R > 8; }
 
 // Persistent stream-K grid: the resident CTAs of one wave.
 static int grid_for(int R, int sm_count, bool tc = false) {
   if (tc) return sm_count;
-  return sm_count * (use_keys_kernel(R) ? keys_ctas_per_sm() : ROWS_CTAS_PER_SM);
+  return sm_count * (use_keys_kernel(R) ? KEYS_CTAS_PER_SM : ROWS_CTAS_PER_SM);
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-// Dynamic chunks per active CTA (MD_DYN_K, default 4; only used by long calls, see make_plan).
-// Keys kernel only: its consumers are lightly loaded and get Q from the producer, so the
-// extra segment boundaries are cheap; the rows kernel (HMMA-heavy consumers that fetch Q at
-// each segment) measured slower with dynamic chunks (Llama verify 1.23 -> 1.34 ms) and its
-// static stream-K spread is small once the epilogue no longer stalls the producer.
-// tcgen05 verify kernel: dynamic chunks per CTA (MD_TC_DYN_K).  Default 0: measured slower
-// (Llama verify 1.24 -> 1.30 ms, Qwen 1.89 -> 2.08 ms with 4): every extra segment costs a Q
-// load, an O^T epilogue and a split merge, more than the per-SM bandwidth spread it removes.
-static int tc_dyn_k() {
-  static const int k = env_int("MD_TC_DYN_K", 0);
-  return k < 0 ? 0 : k;
-}
-static int dyn_k_for(int R) {
-  static const int k = env_int("MD_DYN_K", 4);
-  static const int rows = env_int("MD_DYN_ROWS", 0);  // 1: also the rows kernel (tests, experiments)
-  return (use_keys_kernel(R) || rows) ? (k < 0 ? 0 : k) : 0;
-}
-static int dyn_min_tiles() {  // 128 tiles = 8 MB of K+V per CTA at d = 128 (MD_DYN_MIN)
-  static const int v = env_int("MD_DYN_MIN", 128);
-  return v < 1 ? 1 : v;
-}
-static int dyn_static_permille() {
-  static const int v = env_int("MD_DYN_STATIC", 750);
-  return v < 0 ? 0 : (v > 1000 ? 1000 : v);
-}
+// Dynamic tail of the keys kernel (long calls only, see make_plan): the first DYN_STATIC_PERMILLE
+// of the tile space is split statically, the rest into DYN_K chunks per CTA claimed at run time.
+// Only the keys kernel: the rows kernel (HMMA-heavy consumers that fetch Q at each segment) and
+// the tcgen05 kernel (every extra segment costs a Q load, an O^T epilogue and a split merge)
+// measured slower with claimed chunks (Llama verify 1.23 -> 1.34 ms / 1.24 -> 1.30 ms).
+// Compile-time constants: the library reads no environment variables.
+constexpr int DYN_K = 4;
+constexpr int DYN_MIN_TILES = 128;  // dynamic only when a call has >= 128 tiles (8 MB of K+V) per CTA
+constexpr int DYN_STATIC_PERMILLE = 750;
+static int dyn_k_for(int R) { return use_keys_kernel(R) ? DYN_K : 0; }
 
 // [counters int32: 2 dynamic-chunk counters + MAX_UNITS unit counters][partials fp32 C*2*R*D]
 // [partial lse fp32 C*2*R], C = G*(1+dyn_k) chunks (G static + at most G*dyn_k dynamic).
@@ -1437,7 +1361,7 @@ static size_t workspace_for(int G, int units, int R, int D) {
   (void)units;
   // partial slots for the mma.sync kernels' grid, or the tcgen05 kernel's (1 CTA / SM, dynamic
   // chunks), whichever is larger (the workspace query does not know which kernel will run)
-  const size_t C = std::max((size_t)G * (1 + dyn_k_for(R)), (size_t)device_sm_count() * (1 + tc_dyn_k()));
+  const size_t C = std::max((size_t)G * (1 + dyn_k_for(R)), (size_t)device_sm_count());
   const size_t X = use_keys_kernel(R) ? 0 : (size_t)G * XS_FRAGS * 16 * D * 4;  // rows-kernel scratch
   return COUNTER_BYTES + align256(C * 2 * R * D * 4) + align256(C * 2 * R * 4) + align256(X);
 }
@@ -1512,7 +1436,7 @@ static md_status launch_tc(const TmapSet& tm, const CUtensorMap& qm, const AttnP
   static int done = -1;
   md_status st = set_smem(kern, smem, &done);
   if (st != MD_OK) return st;
-  if (launch_pdl(kern, grid, tc::THREADS, smem, s, tm, qm, p) != cudaSuccess) return check_launch("attn_tc_kernel");
+  if (launch_pdl(kern, grid, tc::Cfg<NP>::THREADS, smem, s, tm, qm, p) != cudaSuccess) return check_launch("attn_tc_kernel");
   return check_launch("attn_tc_kernel");
 }
 
@@ -1535,7 +1459,7 @@ static md_status make_qmap(CUtensorMap* m, const void* q, int B, int T, int Hq, 
 template <int D>
 static md_status launch_dim(const TmapSet& tm, const AttnParams& p, int grid, cudaStream_t s) {
   if (use_keys_kernel(p.R))
-    return keys_ctas_per_sm() == 2 ? launch_keys<D, 4, 2>(tm, p, grid, s) : launch_keys<D, 4, 1>(tm, p, grid, s);
+    return launch_keys<D, 4, KEYS_CTAS_PER_SM>(tm, p, grid, s);
   switch ((p.R + 15) / 16) {
     case 1: return launch_rows<D, 1, 4>(tm, p, grid, s);
     case 2: return launch_rows<D, 2, 2>(tm, p, grid, s);
@@ -1556,8 +1480,9 @@ static md_status check_cache(const md_kv_cache* c, const char* who) {
   return MD_OK;
 }
 
-static unsigned long long* g_trace = nullptr;  // md_debug_trace
-static size_t g_trace_bytes = 0;
+// md_debug_trace: per calling thread (diagnostics only; thread_local keeps calls reentrant)
+static thread_local unsigned long long* g_trace = nullptr;
+static thread_local size_t g_trace_bytes = 0;
 
 struct IndexedArgs {
   const int32_t* idx = nullptr;
@@ -1579,8 +1504,8 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   if (st != MD_OK) return st;
   if (ix.tp != nullptr) {
     MD_REQUIRE(ix.tp->out_peers != nullptr && ix.tp->world >= 1 && ix.tp->rank >= 0 && ix.tp->rank < ix.tp->world &&
-                   ix.tp->world <= 64,
-               MD_ERR_INVALID_ARG, "%s: bad md_tp_out (need out_peers, 0 <= rank < world <= 64)", who);
+                   ix.tp->world <= 32,
+               MD_ERR_INVALID_ARG, "%s: bad md_tp_out (need out_peers, 0 <= rank < world <= 32)", who);
   }
   MD_REQUIRE(q != nullptr && kv_len != nullptr && (out != nullptr || ix.tp != nullptr), MD_ERR_INVALID_ARG,
              "%s: NULL q/kv_len/out", who);
@@ -1590,7 +1515,11 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   // (with tensor-parallel outputs `out` is NULL: every output row goes to ix.tp->out_peers)
   const int g = Hq / c->num_kv_heads;
   const int R = g * T;
-  MD_REQUIRE(R <= 64, MD_ERR_UNSUPPORTED, "%s: g*T = %d > 64 query rows per KV head is not supported", who, R);
+  // the tcgen05 verify kernel (head_dim 128) takes up to 128 query rows per KV head; the
+  // mma.sync kernels (head_dim 64 verify, drafts with g > 8) up to 64
+  const int max_rows = use_tc_kernel(R, c->head_dim, mode) ? 128 : 64;
+  MD_REQUIRE(R <= max_rows, MD_ERR_UNSUPPORTED, "%s: g*T = %d > %d query rows per KV head is not supported", who, R,
+             max_rows);
   const int units = c->batch * c->num_kv_heads;
   MD_REQUIRE(units <= MAX_UNITS, MD_ERR_UNSUPPORTED, "%s: batch * num_kv_heads = %d > %d is not supported", who,
              units, MAX_UNITS);
@@ -1615,14 +1544,16 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
                "%s: k_new / v_new must be non-NULL and 16-byte aligned", who);
     // the keys and tcgen05 kernels write the new rows themselves; the rows kernel (d = 64 verify,
     // MD_TC=0) gets the same rows from a kv_append launch ahead of it
-    fuse_append = (tcg || use_keys_kernel(R)) && env_int("MD_FUSED_APPEND", 1) != 0;
+    fuse_append = tcg || use_keys_kernel(R);
     // a long keys-kernel call (the MHA verify) runs the dynamic tail (make_plan), which the fused
     // append cannot serve (its rows are written per static range): keep the tail and enqueue the
     // append kernel ahead instead (decided on an upper bound of the tile count)
     const int64_t tiles_ub = (int64_t)c->batch * c->num_kv_heads * ((ix.max_keys + TK - 1) / TK);
-    if (fuse_append && !tcg && dyn_k_for(R) > 0 && tiles_ub >= (int64_t)dyn_min_tiles() * grid) fuse_append = false;
-    if (!fuse_append && (st = launch_kv_append(c, ix.k_new, ix.v_new, T, kv_len, -T, s)) != MD_OK) return st;
+    if (fuse_append && !tcg && dyn_k_for(R) > 0 && tiles_ub >= (int64_t)DYN_MIN_TILES * grid) fuse_append = false;
   }
+  // host-side errors must be found before anything is enqueued: the separate append (when the
+  // kernel cannot fuse it) is launched only once every check and tensor map has succeeded
+  const bool separate_append = ix.k_new != nullptr && !fuse_append;
   AttnParams p{};
   p.q = static_cast<const uint16_t*>(q);
   if (fuse_append) {
@@ -1658,16 +1589,15 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.out_hq = ix.tp ? ix.tp->world * Hq : Hq;
   p.out_h0 = ix.tp ? ix.tp->rank * Hq : 0;
   p.trace = (g_trace != nullptr && g_trace_bytes >= (size_t)grid * TRACE_SLOTS * 8) ? g_trace : nullptr;
-  p.fused_merge = fused_merge_enabled();
   p.kc = static_cast<const uint16_t*>(c->k);
   p.vc = static_cast<const uint16_t*>(c->v);
   p.row_sB = c->stride_b / c->head_dim;
   p.row_sH = c->stride_h / c->head_dim;
   p.row_sS = c->stride_s / c->head_dim;
-  p.dyn_k = tcg ? tc_dyn_k() : dyn_k_for(R);  // the tcgen05 kernel's dynamic tail (make_plan)
+  p.dyn_k = tcg ? 0 : dyn_k_for(R);  // dynamic tail: keys kernel only (make_plan)
   if (fuse_append) p.dyn_k = 0;  // the new rows are written per static range (append_own_rows)
-  p.dyn_static_permille = dyn_static_permille();
-  p.dyn_min_tiles = dyn_min_tiles();
+  p.dyn_static_permille = DYN_STATIC_PERMILLE;
+  p.dyn_min_tiles = DYN_MIN_TILES;
   const size_t chunks = (size_t)grid * (1 + p.dyn_k);
   uint8_t* w = static_cast<uint8_t*>(ws);
   p.dyn = reinterpret_cast<int*>(w);
@@ -1678,28 +1608,28 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.ws_lse = reinterpret_cast<float*>(w);
   w += align256(chunks * 2 * R * 4);
   p.ws_x = use_keys_kernel(R) ? nullptr : reinterpret_cast<float*>(w);
-  p.pdl_early = env_int("MD_KEYS_PDL_EARLY", 1);
+  p.pdl_early = 1;  // keys kernel: trigger the dependent launch at entry
   if (tcg) {
     // measured: an entry trigger lets the next kv_append pre-launch and costs ~29 us per
     // verify -> append boundary; triggering at exit makes the appends free (tools/step_probe.py)
-    p.pdl_early = env_int("MD_TC_PDL_EARLY", 0);
+    p.pdl_early = 0;
     CUtensorMap qm;
     if ((st = make_qmap(&qm, q, c->batch, T, Hq, g, c->head_dim)) != MD_OK) return st;
+    if (separate_append && (st = launch_kv_append(c, ix.k_new, ix.v_new, T, kv_len, -T, s)) != MD_OK) return st;
     // the BASELINE shapes get a compile-time row count (Llama-3.1 g=4 x T=5, Qwen2.5 g=7 x T=5)
     st = (R == 20)   ? launch_tc<32, 20>(tm, qm, p, grid, s)
          : (R == 35) ? launch_tc<48, 35>(tm, qm, p, grid, s)
          : (R <= 16) ? launch_tc<16, 0>(tm, qm, p, grid, s)
          : (R <= 32) ? launch_tc<32, 0>(tm, qm, p, grid, s)
-                     : launch_tc<48, 0>(tm, qm, p, grid, s);
+         : (R <= 48) ? launch_tc<48, 0>(tm, qm, p, grid, s)
+         : (R <= 64) ? launch_tc<64, 0>(tm, qm, p, grid, s)
+         : (R <= 96) ? launch_tc<96, 0>(tm, qm, p, grid, s)
+                     : launch_tc<128, 0>(tm, qm, p, grid, s);
   } else {
+    if (separate_append && (st = launch_kv_append(c, ix.k_new, ix.v_new, T, kv_len, -T, s)) != MD_OK) return st;
     st = (c->head_dim == 128) ? launch_dim<128>(tm, p, grid, s) : launch_dim<64>(tm, p, grid, s);
   }
-  if (st != MD_OK || p.fused_merge) return st;
-  if (c->head_dim == 128)
-    launch_pdl(attn_merge_kernel<128>, dim3(units), dim3(128), 0, s, p, grid);
-  else
-    launch_pdl(attn_merge_kernel<64>, dim3(units), dim3(128), 0, s, p, grid);
-  return check_launch("attn_merge_kernel");
+  return st;
 }
 
 }  // namespace md

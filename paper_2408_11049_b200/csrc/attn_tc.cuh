@@ -1,19 +1,21 @@
 // attn_tc.cuh — the tcgen05 (5th-generation tensor core) verify kernel, included by attn.cu
 // after the stream-K machinery (AttnParams, Plan, SegWalker, finish_unit) it reuses.
 //
-// md_verify_attn_full for R = g*(gamma+1) in (8, 48] query rows per KV head at head_dim 128
-// (GQA verify: Llama-3.1 R = 20, Qwen2.5 R = 35).  Swapped operands so
+// md_verify_attn_full for R = g*(gamma+1) in (8, 128] query rows per KV head at head_dim 128
+// (GQA verify: Llama-3.1 R = 20, Qwen2.5 R = 35; up to gamma = 15 with g = 8, or Qwen2.5 (g = 7)
+// to gamma = 15 = 112 rows; SURVEY §8(a) row a3, §8(b) g*T <= 128).  Swapped operands so
 // the tensor-core work is 2 * 128 * NP FLOP per key (NP = R rounded up to 16), not 128 rows:
 //   S^T[128 keys][NP]  = K[128 keys][d] . Q^T            (A = K tile, K-major SW128 from TMA;
 //                                                          B = Q rows, K-major SW128 from TMA)
 //   O^T[d][NP]        += V^T . P^T                       (A = V tile read MN-major, SW128;
 //                                                          B = P^T, MN-major 8x8 core matrices)
-// Both accumulators live in TMEM (S^T double-buffered by tile, O^T by segment).  Warp roles
-// (192 threads, 1 CTA / SM, 3 x 64 KB K/V stages of 128 keys):
-//   warp 4  TMA producer: the segment's Q rows (one 3-D box per 64-column slab) and K/V tiles;
-//   warp 5  MMA issuer (one thread) + TMEM allocator: S^T(i) is issued before PV(i-1);
-//   warps 0-3 softmax + epilogue, thread x <-> TMEM lane x (key x of the tile for S^T, head
-//           dim x for O^T): each thread owns one key's NP scores, so the online softmax needs
+// Both accumulators live in TMEM (S^T double-buffered by tile, O^T by segment: 4 NP <= 512
+// columns).  Warp roles (1 CTA / SM, 3 x 64 KB K/V stages of 128 keys; 2 stages above NP = 48):
+//   warp 4NG    TMA producer: the segment's Q rows (one 3-D box per 64-column slab) and K/V tiles;
+//   warp 4NG+1  MMA issuer (one thread) + TMEM allocator: S^T(i) is issued before PV(i-1);
+//   warps 0..4NG-1 softmax + epilogue in NG row groups of 4 warps (NG = 1 up to NP = 48, else
+//           NP / 32 groups of 32 rows), thread x of a group <-> TMEM lane x (key x of the tile
+//           for S^T, head dim x for O^T): each thread owns one key's scores for the group's rows, so the online softmax needs
 //           no cross-thread work per tile except a CTA vote: the running row maxima m are only
 //           raised when a score exceeds m + 8 (log2 units; P stays <= 2^8, exact in the
 //           fp32 sums and a bf16 operand like any other), which rescales the thread-local row
@@ -29,33 +31,43 @@ constexpr int KT = 128;                      // keys per stage (MMA M)
 constexpr int SLAB = KT * 128;               // one 64-column slab of a 128-key tile
 constexpr int STAGE = 4 * SLAB;              // K (2 slabs) + V (2 slabs) = 64 KB
 constexpr float THR = 8.f;                   // lazy max-raise threshold (log2 units)
-constexpr int SM_THREADS = 128;              // softmax / epilogue threads
-constexpr int THREADS = SM_THREADS + 64;     // + producer warp + MMA warp
+constexpr int SMEM_MAX = 232448;             // 227 KB per CTA
 
+// NP = R rounded up to 16 query-row columns (<= 128: S^T x2 + O^T x2 = 4 NP <= 512 TMEM columns).
+// Up to 48 columns one group of 128 softmax threads holds every row's state in registers; above
+// that the rows are cut into NG groups of CW = 32 columns, each group a further 4 warps over the
+// same 128 TMEM lanes (warp w reads lane quadrant w % 4), so the per-thread state stays at 32 rows.
 template <int NP>
 struct Cfg {
+  static constexpr int NG = NP <= 48 ? 1 : NP / 32;  // row groups
+  static constexpr int CW = NP / NG;                 // query-row columns per group
+  static constexpr int SM_THREADS = 128 * NG;        // softmax / epilogue threads
+  static constexpr int THREADS = SM_THREADS + 64;    // + producer warp + MMA warp
   static constexpr int NQ = NP <= 32 ? 2 : 1;        // Q buffers (by segment parity)
   static constexpr int QBUF = 2 * NP * 128;          // Q rows, two 64-column SW128 slabs
   static constexpr int PBUF = NP * KT * 2;           // P^T, 8x8 core matrices
-  static constexpr int NSTAGE = 3;
-  static constexpr int AUX = 2048 + TABLE_BYTES;     // barriers, tmem slot, row state, plan
-  static constexpr int SMEM = NSTAGE * STAGE + NQ * QBUF + PBUF + AUX + 1024;
-  static constexpr int TMEM_COLS = 4 * NP <= 128 ? 128 : 256;  // S^T x2 + O^T x2
-  static_assert(SMEM <= 232448, "shared memory budget");
+  static constexpr int AUX = 1024 + 6 * NP * 4;      // barriers, tmem slot, flags, plan; red[4NG][CW], mrow, crow
+  static constexpr int FIXED = NQ * QBUF + PBUF + AUX + TABLE_BYTES + 1024;
+  static constexpr int NSTAGE = (3 * STAGE + FIXED <= SMEM_MAX) ? 3 : 2;
+  static constexpr int SMEM = NSTAGE * STAGE + FIXED;
+  static constexpr int TMEM_COLS = 4 * NP <= 128 ? 128 : (4 * NP <= 256 ? 256 : 512);
+  static_assert(NP % 16 == 0 && NP >= 16 && NP <= 128, "16 <= NP <= 128, a multiple of 16");
+  static_assert(NG == 1 || CW == 32, "groups of 32 columns");
+  static_assert(SMEM <= SMEM_MAX, "shared memory budget");
 };
 
-// OR-vote over the 128 softmax threads (named barrier 2)
-__device__ __forceinline__ bool vote_any128(bool v) {
+// OR-vote over the 128 softmax threads of a row group (named barrier `id`)
+__device__ __forceinline__ bool vote_any128(bool v, int id = 2) {
   uint32_t r;
   asm volatile(
-      "{\n\t.reg .pred q, p;\n\tsetp.ne.u32 q, %1, 0;\n\tbarrier.cta.red.or.pred p, 2, 128, q;\n\t"
+      "{\n\t.reg .pred q, p;\n\tsetp.ne.u32 q, %1, 0;\n\tbarrier.cta.red.or.pred p, %2, 128, q;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(r)
-      : "r"((uint32_t)v)
+      : "r"((uint32_t)v), "r"(id)
       : "memory");
   return r != 0;
 }
-__device__ __forceinline__ void bar128() { named_bar_sync(2, SM_THREADS); }
+__device__ __forceinline__ void bar128(int id = 2) { named_bar_sync(id, 128); }
 
 // diagnostics (md_debug_trace): cycles spent in a wait, accumulated by one thread
 __device__ __forceinline__ void twait(uint64_t* bar, uint32_t parity, long long* acc) {
@@ -153,11 +165,24 @@ __device__ void produce(const AttnParams& p, const TmapSet& tm, const CUtensorMa
   }
 }
 
+// Zero key x's V row of a stage (cache rows past the valid keys may hold NaN bits).  The 16-byte
+// chunks are visited in a lane-rotated order, so the 8 lanes of a quarter-warp store to 8
+// different bank groups (the rows are 128 bytes apart: the same chunk order would be 8-way).
+__device__ __forceinline__ void zero_vrow(uint8_t* vrow, int x) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int cc = (c + x) & 7;
+    *reinterpret_cast<uint4*>(vrow + cc * 16) = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(vrow + SLAB + cc * 16) = make_uint4(0, 0, 0, 0);
+  }
+}
+
 // RR > 0: the row count R is a compile-time constant (the hot configurations), else p.R
 template <int NP, int RR>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     attn_tc_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ CUtensorMap qmap, const AttnParams p) {
   using C = Cfg<NP>;
+  constexpr int NG = C::NG, CW = C::CW, SM_THREADS = C::SM_THREADS;
   const int R = RR > 0 ? RR : p.R;
   constexpr int NSTAGE = C::NSTAGE, NQ = C::NQ;
   constexpr int D = 128;
@@ -176,21 +201,19 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* pempty = pfull + 1;      // [1]
   uint64_t* ofull = pempty + 1;      // [2]
   uint64_t* oempty = ofull + 2;      // [2]
-  uint64_t* cfull = oempty + 2;      // [2] dynamic chunk hand-off, producer -> MMA + softmax
-  uint64_t* cempty = cfull + 2;      // [2]
-  uint64_t* vfull = cempty + 2;      // [NSTAGE] V halves of the ring stages (full / empty: K halves)
+  uint64_t* vfull = oempty + 2;      // [NSTAGE] V halves of the ring stages (full / empty: K halves)
   uint64_t* vempty = vfull + NSTAGE; // [NSTAGE]
-  uint64_t* apb = vempty + NSTAGE;   // [1] fused append: the softmax warps' new-row stores are done
-  int* cids = reinterpret_cast<int*>(apb + 1);  // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(cids + 2);
+  uint64_t* apb = vempty + NSTAGE;   // [1] fused append: the group-0 softmax warps' new-row stores are done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(apb + 1);
   int* flag = reinterpret_cast<int*>(tslot + 4);                 // [16] finish_unit
   Plan* plan_smem = reinterpret_cast<Plan*>(flag + 16);          // 40 bytes (reserved 64)
-  float* red = reinterpret_cast<float*>(flag + 32);              // [4][NP] per-warp row maxima / sums
+  float* red = reinterpret_cast<float*>(smem + NSTAGE * STAGE + NQ * C::QBUF + C::PBUF + 1024);  // [4NG][CW]
   float* mrow = red + 4 * NP;                                    // [NP] running row maxima (log2 units)
-  float* crow = mrow + NP;                                       // [NP] rescale factors
+  float* crow = mrow + NP;                                       // [NP] rescale factors / row sums
   int* pre = reinterpret_cast<int*>(crow + NP);                  // [TABLE_B + 1]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int PRODUCER = 4 * NG, ISSUER = 4 * NG + 1;  // warp roles after the softmax warps
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
@@ -202,31 +225,27 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&qfull[s], 1);
       mbar_init(&qempty[s], 1);
       mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 4);
+      mbar_init(&sempty[s], 4 * NG);
       mbar_init(&ofull[s], 1);
-      mbar_init(&oempty[s], 4);
+      mbar_init(&oempty[s], 4 * NG);
     }
-    mbar_init(pfull, 4);
+    mbar_init(pfull, 4 * NG);
     mbar_init(pempty, 1);
-    for (int s2 = 0; s2 < 2; ++s2) {
-      mbar_init(&cfull[s2], 1);
-      mbar_init(&cempty[s2], 5);  // the MMA thread + one arrival per softmax warp
-    }
     mbar_init(apb, 4);
     fence_mbar_init();
   }
   // Q rows >= R stay zero for the whole kernel (the TMA boxes write rows < R only)
-  for (int i = threadIdx.x; i < NQ * C::QBUF / 16; i += THREADS) {
+  for (int i = threadIdx.x; i < NQ * C::QBUF / 16; i += C::THREADS) {
     const int slab_row = (i * 16 / 128) % NP;
     if (slab_row >= p.R) reinterpret_cast<uint4*>(qbuf)[i] = make_uint4(0, 0, 0, 0);
   }
   fence_proxy_async();
-  if (warp == 5) {
+  if (warp == ISSUER) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
                  "n"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (warp == 4 && lane == 0) {  // descriptor fetches overlap the grid-dependency wait
+  if (warp == PRODUCER && lane == 0) {  // descriptor fetches overlap the grid-dependency wait
     prefetch_tmap(&tm.k_full);
     prefetch_tmap(&tm.v_full);
     prefetch_tmap(&tm.k_part);
@@ -242,58 +261,33 @@ __global__ void __launch_bounds__(THREADS, 1)
   build_prefix(p, pre);
   if (threadIdx.x == 0) *plan_smem = make_plan(p, total_tiles(p, pre), gridDim.x);
   __syncthreads();
-  const Plan& pl = *plan_smem;
-  int chunk = blockIdx.x;  // this CTA's static chunk, then the dynamic ones its producer claims
+  const Plan& pl = *plan_smem;  // static stream-K plan (the host sets dyn_k = 0 for this kernel)
+  const int chunk = blockIdx.x;
   const bool active = (int)blockIdx.x < pl.G;
   SegWalker walk;
   Seg sg;
   if (active) walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
   if (p.kn != nullptr && warp < 4 && active) {  // fused append: the new rows of this CTA's tiles
-    append_own_rows<128>(p, pre, pl.start(chunk), pl.start(chunk + 1), threadIdx.x, SM_THREADS);
+    append_own_rows<128>(p, pre, pl.start(chunk), pl.start(chunk + 1), threadIdx.x, 128);
     __syncwarp();
     if (lane == 0) mbar_arrive(apb);
   }
 
-  if (warp == 4) {
+  if (warp == PRODUCER) {
     // ============================== TMA producer ==============================
     if (active && lane == 0) {
-      prefetch_tmap(&tm.k_full);
-      prefetch_tmap(&tm.v_full);
-      prefetch_tmap(&tm.k_part);
-      prefetch_tmap(&tm.v_part);
-      prefetch_tmap(&qmap);
       const uint64_t pol = policy_evict_first();
-      int it = 0, qi = 0, ck = 0;
+      int it = 0, qi = 0;
       PendV pend{-1, 0, 0, 0, 0};
       long long tw = 0;
       long long* twp = p.trace ? &tw : nullptr;
-      // dynamic tail (long calls, see make_plan): chunks claimed one ahead from an atomic
-      // counter and handed to the MMA and softmax roles through a 2-slot mbarrier ring
-      int ahead = 0;
-      if (pl.nch > pl.G) ahead = atomicAdd(p.dyn, 1);
-      while (true) {
-        if (!walk.next(p, pre, sg)) {
-          if (pl.nch == pl.G) break;
-          const int c = pl.G + ahead;
-          const int nxt = c < pl.nch ? c : -1;
-          if (nxt >= 0) ahead = atomicAdd(p.dyn, 1);
-          const int cs = ck & 1;
-          mbar_wait(&cempty[cs], ((ck >> 1) & 1) ^ 1);
-          cids[cs] = nxt;
-          mbar_arrive(&cfull[cs]);
-          ++ck;
-          if (nxt < 0) break;
-          chunk = nxt;
-          walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
-          continue;
-        }
+      while (walk.next(p, pre, sg))
         produce<NP>(p, tm, &qmap, sg, seg_ranges(p, sg), ring, qbuf, full, empty, vfull, vempty, qfull, qempty, it, qi,
                     pend, pol, twp, apb);
-      }
       if (pend.it >= 0) issue_v<NSTAGE>(tm, ring, vfull, vempty, pend, pol);
       if (p.trace) trace_put(p, 15, tw);
     }
-  } else if (warp == 5) {
+  } else if (warp == ISSUER) {
     // ============================== MMA issuer ==============================
     if (active && lane == 0) {
       constexpr uint32_t ID_S = idesc(128, NP, 0, 0), ID_O = idesc(128, NP, 1, 1);
@@ -304,7 +298,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       long long* ws_ = p.trace ? &w_se : nullptr;
       long long* wp = p.trace ? &w_pf : nullptr;
       // the PV of the previous tile is issued after this tile's S^T (S^T double-buffered)
-      int pv_stage = -1, pv_ob = 0, pv_first = 0, pv_last = 0, pv_qs = 0, pv_tt = 0, pv_it = 0;
+      int pv_stage = -1, pv_ob = 0, pv_first = 0, pv_last = 0, pv_tt = 0, pv_it = 0;
       auto issue_pv = [&]() {
         mbar_wait(&vfull[pv_stage], (pv_it / NSTAGE) & 1);
         twait(pfull, pv_tt & 1, wp);
@@ -320,22 +314,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (pv_last) commit(&ofull[pv_ob]);
         pv_stage = -1;
       };
-      int ck = 0;
-      auto next_seg = [&]() -> bool {  // mirrors the producer's chunk sequence
-        while (!walk.next(p, pre, sg)) {
-          if (pl.nch == pl.G) return false;
-          const int cs = ck & 1;
-          mbar_wait(&cfull[cs], (ck >> 1) & 1);
-          const int nxt = cids[cs];
-          mbar_arrive(&cempty[cs]);
-          ++ck;
-          if (nxt < 0) return false;
-          chunk = nxt;
-          walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
-        }
-        return true;
-      };
-      while (next_seg()) {
+      while (walk.next(p, pre, sg)) {
         const Ranges rg = seg_ranges(p, sg);
         const int ns = seg_stages(rg);
         const int qs = qi % NQ, ob = si & 1;
@@ -362,7 +341,6 @@ __global__ void __launch_bounds__(THREADS, 1)
           pv_ob = ob;
           pv_first = (j == 0);
           pv_last = (j == ns - 1);
-          pv_qs = qs;
           pv_tt = tt;
           pv_it = it;
         }
@@ -370,7 +348,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         ++si;
       }
       if (pv_stage >= 0) issue_pv();
-      (void)pv_qs;
       if (p.trace) {
         trace_put(p, 8, w_full);
         trace_put(p, 9, w_se);
@@ -378,40 +355,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         trace_put(p, 11, tt);
       }
     }
-  } else if (active) {
-    // ============================== softmax + epilogue (128 threads) ==============================
+  } else if (active && NG == 1) {
+    // ====================== softmax + epilogue, all rows in one group (NP <= 48) ======================
     const int x = threadIdx.x;                      // TMEM lane: key of the tile / head-dim row of O^T
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     int it = 0, tt = 0, si = 0;
     long long w_sf = 0, w_pe = 0, w_epi = 0, t_start = clock64();
     long long* wsf = (p.trace && x == 0) ? &w_sf : nullptr;
     long long* wpe = (p.trace && x == 0) ? &w_pe : nullptr;
-    long long sec[6] = {0, 0, 0, 0, 0, 0}, tsec = 0;
-    const bool prof = p.trace && x == 0;
-#define TSEC(k)                              \
-  if (prof) {                                \
-    const long long tn = clock64();          \
-    sec[k] += tn - tsec;                     \
-    tsec = tn;                               \
-  }
     float mr[NP], lacc[NP];
-    int ck = 0;
-    auto next_seg = [&]() -> bool {  // mirrors the producer's chunk sequence
-      while (!walk.next(p, pre, sg)) {
-        if (pl.nch == pl.G) return false;
-        const int cs = ck & 1;
-        mbar_wait(&cfull[cs], (ck >> 1) & 1);
-        const int nxt = cids[cs];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&cempty[cs]);
-        ++ck;
-        if (nxt < 0) return false;
-        chunk = nxt;
-        walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
-      }
-      return true;
-    };
-    while (next_seg()) {
+    while (walk.next(p, pre, sg)) {
       const int b = sg.b, kvh = sg.kvh, n = sg.n;
       const Ranges rg = seg_ranges(p, sg);
       const int ns = seg_stages(rg);
@@ -431,7 +384,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int key = pos + x;                    // cache position (verify)
         const bool valid = x < nvalid;
         twait(&sfull[sb], (tt >> 1) & 1, wsf);
-        if (prof) tsec = clock64();
         fence_after();
         float v[NP];
 #pragma unroll
@@ -440,7 +392,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[sb]);
-        TSEC(0)
         // x_r = s_r * scale * log2(e) - m_r: one FMA per row, reused for the raise test and
         // the exponent.  Masking (keys past the valid range; the causal chain / tree mask among
         // the T new keys) only exists in a unit's last stage: a tile-uniform branch.
@@ -473,10 +424,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
         const bool need = xmax > THR;  // some score exceeds its row maximum by > 2^8 (or m = -inf)
-        TSEC(1)
         // the previous tile's PV must be complete before P is rewritten or O^T rescaled
         if (tt > 0) twait(pempty, (tt - 1) & 1, wpe);
-        if (prof) tsec = clock64();
         if (vote_any128(need)) {
           // raise every row's maximum to this tile's (or keep it): per-row max over the tile
 #pragma unroll
@@ -520,7 +469,6 @@ __global__ void __launch_bounds__(THREADS, 1)
             wait_st();
           }
         }
-        TSEC(2)
         // P = 2^x; row sums accumulate in fp32, the MMA operand is bf16
         uint32_t pk[NP / 2];
 #pragma unroll
@@ -530,30 +478,22 @@ __global__ void __launch_bounds__(THREADS, 1)
           lacc[r + 1] += p1;
           pk[r / 2] = pack_bf16(p0, p1);
         }
-        TSEC(3)
         // P^T core layout: key x -> core column x / 8, row (x % 8) * 16 B; rows r -> core r / 8
         uint8_t* pd = pbuf + (x >> 3) * 128 + (x & 7) * 16;
 #pragma unroll
         for (int c = 0; c < NP / 8; ++c)
           *reinterpret_cast<uint4*>(pd + c * 2048) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        if (!valid) {  // zero this key's V row (cache rows past the valid keys may hold NaN bits)
-          mbar_wait(&vfull[stage], (it / NSTAGE) & 1);  // after the V half's TMA writes land
-          uint8_t* vrow = ring + stage * STAGE + 2 * SLAB + x * 128;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            *reinterpret_cast<uint4*>(vrow + c * 16) = make_uint4(0, 0, 0, 0);
-            *reinterpret_cast<uint4*>(vrow + SLAB + c * 16) = make_uint4(0, 0, 0, 0);
-          }
+        if (!valid) {  // zero this key's V row (after the V half's TMA writes land)
+          mbar_wait(&vfull[stage], (it / NSTAGE) & 1);
+          zero_vrow(ring + stage * STAGE + 2 * SLAB + x * 128, x);
         }
-        TSEC(4)
         fence_proxy_async();
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(pfull);
-        TSEC(5)
       }
       // ---------------- segment epilogue: row sums over the 128 key lanes, O^T / l
-      const long long t_epi = prof ? clock64() : 0;
+      const long long t_epi = p.trace ? clock64() : 0;
 #pragma unroll
       for (int r = 0; r < NP; ++r) {
         float l = lacc[r];
@@ -593,9 +533,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           __stcg(p.ws_lse + (int64_t)slot_base * p.R + x, lse2);
         }
       }
-      if (!complete && p.fused_merge) finish_unit<D>(p, sg, pl, SM_THREADS, flag);
+      if (!complete) finish_unit<D>(p, sg, pl, SM_THREADS, flag);
       bar128();  // red / mrow / crow reused by the next segment
-      if (prof) w_epi += clock64() - t_epi;
+      if (p.trace) w_epi += clock64() - t_epi;
       ++si;
     }
     if (p.trace && x == 0) {
@@ -604,22 +544,190 @@ __global__ void __launch_bounds__(THREADS, 1)
       trace_put(p, 14, clock64() - t_start);
       trace_put(p, 7, w_epi);  // segment epilogues (row sums, O^T read, stores, split merge)
       trace_put(p, 6, globaltimer());  // softmax end (ns): the CTA's finish time
-      for (int k = 0; k < 6; ++k) trace_put(p, k, sec[k]);
     }
-#undef TSEC
-  }
-  // the last CTA to finish re-arms the dynamic counters for the next call (every producer has
-  // made its final claim before any role saw the -1 hand-off)
-  if (active && pl.nch > pl.G && threadIdx.x == 0) {
-    if (atomicAdd(p.dyn + 1, 1) == pl.G - 1) {
-      p.dyn[0] = 0;
-      p.dyn[1] = 0;
+  } else if (active) {
+    // ============ softmax + epilogue, row group g of NG (CW = 32 columns [cb, cb + CW)) ============
+    const int x = threadIdx.x & 127;                // TMEM lane: key of the tile / head-dim row of O^T
+    const int grp = threadIdx.x >> 7, wq = warp & 3, cb = grp * CW;
+    const int bar_id = 2 + grp;                     // the group's named barrier
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    float* gred = red + grp * 4 * CW;               // [4][CW] per-warp row partials of this group
+    int it = 0, tt = 0, si = 0;
+    float lacc[CW];
+    while (walk.next(p, pre, sg)) {
+      const int b = sg.b, kvh = sg.kvh, n = sg.n;
+      const Ranges rg = seg_ranges(p, sg);
+      const int ns = seg_stages(rg);
+      const int ob = si & 1;
+      const int vbase = n - p.T;
+#pragma unroll
+      for (int r = 0; r < CW; ++r) lacc[r] = 0.f;
+      if (x < CW) mrow[cb + x] = -INFINITY;
+      bar128(bar_id);
+      for (int j = 0; j < ns; ++j, ++it, ++tt) {
+        const int stage = it % NSTAGE, sb = tt & 1;
+        const int pos = rg.s0 + j * KT;
+        const int nvalid = min(KT, rg.e0 - pos);
+        const bool valid = x < nvalid;
+        const bool edge = (nvalid < KT) || (pos + KT > vbase);
+        const int rel = pos + x - vbase;
+        const float sl2 = p.scale_log2;
+        const uint32_t s_col = tbase + sb * NP + cb + lane_off;
+        // hidden(r): key x is invisible to query row cb + r (past the valid keys, or a new key
+        // outside the row's causal chain / tree mask); only an edge stage hides anything
+        uint32_t hid = 0;  // bit r set: hidden
+        if (edge) {
+          int t = cb / p.g, hh = cb - t * p.g;
+          uint32_t msk = t < p.T ? (p.tree_mask ? __ldg(p.tree_mask + (size_t)b * p.T + t) : ((2u << t) - 1u)) : 0u;
+#pragma unroll
+          for (int r = 0; r < CW; ++r) {
+            if (!valid || (rel >= 0 && !((msk >> (rel & 31)) & 1u))) hid |= 1u << r;
+            if (++hh == p.g) {
+              hh = 0;
+              ++t;
+              if (t < p.T) msk = p.tree_mask ? __ldg(p.tree_mask + (size_t)b * p.T + t) : ((2u << t) - 1u);
+            }
+          }
+        }
+        twait(&sfull[sb], (tt >> 1) & 1, nullptr);
+        fence_after();
+        float xs[CW];
+        tld16(s_col, xs);
+        tld16(s_col + 16, xs + 16);
+        wait_ld();
+        float xmax = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < CW; r += 4) {
+          const float4 m4 = *reinterpret_cast<const float4*>(mrow + cb + r);
+          const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const bool live = (cb + r + i < R) && !((hid >> (r + i)) & 1u);
+            xs[r + i] = live ? fmaf(xs[r + i], sl2, -mm[i]) : -INFINITY;
+            xmax = fmaxf(xmax, xs[r + i]);
+          }
+        }
+        const bool need = xmax > THR;  // a score exceeds its row maximum by > 2^8 (or m = -inf)
+        if (tt > 0) twait(pempty, (tt - 1) & 1, nullptr);  // previous PV done: P and O^T are free
+        if (vote_any128(need, bar_id)) {
+          // the scores are still in S^T (this group has not released the buffer): reload them
+          float v[CW];
+          tld16(s_col, v);
+          tld16(s_col + 16, v + 16);
+          wait_ld();
+#pragma unroll
+          for (int r = 0; r < CW; ++r) {
+            const bool live = (cb + r < R) && !((hid >> r) & 1u);
+            v[r] = live ? v[r] * sl2 : -INFINITY;  // scaled score (log2 units)
+            float m = v[r];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) gred[wq * CW + r] = m;
+          }
+          bar128(bar_id);
+          if (x < CW) {
+            const float m = fmaxf(fmaxf(gred[x], gred[CW + x]), fmaxf(gred[2 * CW + x], gred[3 * CW + x]));
+            const float mo = mrow[cb + x];
+            const float mn = fmaxf(mo, m);
+            crow[cb + x] = (mo == -INFINITY) ? 0.f : ex2(mo - mn);
+            mrow[cb + x] = mn;
+          }
+          bar128(bar_id);
+#pragma unroll
+          for (int r = 0; r < CW; ++r) {
+            const float mn = mrow[cb + r];
+            lacc[r] *= crow[cb + r];
+            xs[r] = (v[r] == -INFINITY) ? -INFINITY : v[r] - ((mn == -INFINITY) ? 0.f : mn);
+          }
+          if (j > 0) {  // O^T already holds PV of earlier tiles of this segment: rescale it
+            const uint32_t oa = tbase + 2 * NP + ob * NP + cb + lane_off;
+#pragma unroll
+            for (int c = 0; c < CW; c += 16) {
+              float o[16];
+              tld16(oa + c, o);
+              wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] *= (cb + c + i < R) ? crow[cb + c + i] : 0.f;
+              tst16(oa + c, o);
+            }
+            wait_st();
+          }
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[sb]);  // S^T buffer sb is free (also after a reload)
+        // P = 2^x for the group's rows; row sums in fp32, the MMA operand is bf16
+        uint32_t pk[CW / 2];
+#pragma unroll
+        for (int r = 0; r < CW; r += 2) {
+          const float p0 = ex2(xs[r]), p1 = ex2(xs[r + 1]);  // ex2(-inf) = 0 for hidden / padded rows
+          lacc[r] += p0;
+          lacc[r + 1] += p1;
+          pk[r / 2] = pack_bf16(p0, p1);
+        }
+        uint8_t* pd = pbuf + (x >> 3) * 128 + (x & 7) * 16 + (cb / 8) * 2048;
+#pragma unroll
+        for (int c = 0; c < CW / 8; ++c)
+          *reinterpret_cast<uint4*>(pd + c * 2048) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        if (!valid && grp == 0) {  // zero this key's V row once (after the V half's TMA writes land)
+          mbar_wait(&vfull[stage], (it / NSTAGE) & 1);
+          zero_vrow(ring + stage * STAGE + 2 * SLAB + x * 128, x);
+        }
+        fence_proxy_async();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(pfull);
+      }
+      // ---------------- segment epilogue: the group's row sums, O^T / l
+#pragma unroll
+      for (int r = 0; r < CW; ++r) {
+        float l = lacc[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+        if (lane == 0) gred[wq * CW + r] = l;
+      }
+      bar128(bar_id);
+      if (x < CW) crow[cb + x] = gred[x] + gred[CW + x] + gred[2 * CW + x] + gred[3 * CW + x];  // L_r
+      mbar_wait(&ofull[ob], (si >> 1) & 1);
+      fence_after();
+      float o[CW];
+      tld16(tbase + 2 * NP + ob * NP + cb + lane_off, o);
+      tld16(tbase + 2 * NP + ob * NP + cb + 16 + lane_off, o + 16);
+      wait_ld();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&oempty[ob]);
+      bar128(bar_id);
+      const bool complete = sg.complete();
+      const int slot_base = chunk * 2 + pl.slot(sg.ustart, chunk);
+#pragma unroll
+      for (int r = 0; r < CW; ++r) {
+        const int row = cb + r;
+        if (row < R) {
+          const float L = crow[row];
+          const float val = (L > 0.f) ? o[r] / L : 0.f;
+          if (complete) store_out(p, o_row(p, b, kvh, row) * D + x, val);
+          else __stcg(p.ws_o + ((int64_t)slot_base * p.R + row) * D + x, val);
+        }
+      }
+      if (x < CW && cb + x < R) {
+        const float L = crow[cb + x], m = mrow[cb + x];
+        const float lse2 = (L > 0.f) ? m + __log2f(L) : -INFINITY;
+        if (complete) {
+          if (p.lse != nullptr) p.lse[out_row(p, b, kvh, cb + x)] = lse2 * LN2;
+        } else {
+          __stcg(p.ws_lse + (int64_t)slot_base * p.R + cb + x, lse2);
+        }
+      }
+      if (!complete) finish_unit<D>(p, sg, pl, SM_THREADS, flag);
+      bar128(bar_id);  // the group's red / mrow / crow entries are reused by the next segment
+      ++si;
     }
   }
   fence_before();
   __syncthreads();
   if (!p.pdl_early) pdl_trigger();
-  if (warp == 5) {
+  if (warp == ISSUER) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::TMEM_COLS));
   }

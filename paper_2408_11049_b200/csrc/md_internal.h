@@ -48,10 +48,12 @@ md_status launch_kv_append(const md_kv_cache* c, const void* k_new, const void* 
   } while (0)
 
 namespace md {
-// Launch with the programmatic-stream-serialization attribute (PDL) unless MD_PDL=0: the
-// kernel may start while its predecessor drains; every md kernel calls griddepcontrol.wait
-// before reading anything a predecessor may have written.
-bool pdl_enabled();
+// Launch with the programmatic-stream-serialization attribute (PDL): the kernel may start
+// while its predecessor drains; every md kernel calls griddepcontrol.wait before reading
+// anything a predecessor may have written.  (Compile with -DMD_NO_PDL=1 for plain launches.)
+#ifndef MD_NO_PDL
+#define MD_NO_PDL 0
+#endif
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
@@ -64,7 +66,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = MD_NO_PDL ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 }  // namespace md

@@ -720,14 +720,6 @@ static md_status snap_tc_launch(const md_kv_cache* c, const void* q_obs, const s
   return check_launch("snap_tc_kernel");
 }
 
-static bool snap_tc_enabled() {  // MD_SNAP_TC=0: the mma.sync passes
-  static const bool v = [] {
-    const char* e = getenv("MD_SNAP_TC");
-    return !(e && atoi(e) == 0);
-  }();
-  return v;
-}
-
 }  // namespace md
 
 extern "C" MD_API size_t md_snapkv_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads, int32_t w,
@@ -791,15 +783,12 @@ extern "C" MD_API md_status md_snapkv_select(const md_kv_cache* c, const void* q
   p.budgets = budgets;
   cudaStream_t s = (cudaStream_t)stream;
   const unsigned grid = static_cast<unsigned>(units * p.nchunks);
-  if (c->head_dim == 128 && snap_tc_enabled()) {
+  if (c->head_dim == 128) {  // tcgen05 scoring passes (the mma.sync passes serve head_dim 64)
     p.nchunks = (max_prefill_len + snaptc::CHUNK - 1) / snaptc::CHUNK;  // <= the workspace's chunk count
     const unsigned grid_tc = static_cast<unsigned>(units * p.nchunks);
     const md_status st = (p.R <= 128) ? snap_tc_launch<1>(c, q_obs, p, grid_tc, s)
                                    : snap_tc_launch<2>(c, q_obs, p, grid_tc, s);
     if (st != MD_OK) return st;
-  } else if (c->head_dim == 128) {
-    launch_pdl(snap::lse_kernel<128>, dim3(grid), dim3(snap::THREADS), 0, s, p);
-    launch_pdl(snap::vote_kernel<128>, dim3(grid), dim3(snap::THREADS), 0, s, p);
   } else {
     launch_pdl(snap::lse_kernel<64>, dim3(grid), dim3(snap::THREADS), 0, s, p);
     launch_pdl(snap::vote_kernel<64>, dim3(grid), dim3(snap::THREADS), 0, s, p);

@@ -56,7 +56,16 @@ def test_host_side_validation_without_gpu():
     st, msg = _err(lib.md_verify_attn_full(ctypes.byref(c), 16, 3, 5, 16, 64, 0.1, 16, None, None, 0, None))
     assert st == md.MD_ERR_INVALID_ARG and "multiple" in msg
     st, msg = _err(lib.md_verify_attn_full(ctypes.byref(c), 16, 64, 5, 16, 64, 0.1, 16, None, None, 0, None))
-    assert st == md.MD_ERR_UNSUPPORTED and "64" in msg               # g*T = 32*5 rows
+    assert st == md.MD_ERR_UNSUPPORTED and "128" in msg              # g*T = 32*5 rows
+    # g*T up to 128 rows per KV head (head_dim 128) passes the row check; with no
+    # workspace the call then fails on the workspace, before anything is enqueued
+    st, msg = _err(lib.md_verify_attn_full(ctypes.byref(c), 16, 32, 8, 16, 64, 0.1, 16, None, None, 0, None))
+    assert st == md.MD_ERR_WORKSPACE, msg                             # g*T = 16*8 = 128 rows
+    st, msg = _err(lib.md_verify_attn_full(ctypes.byref(c), 16, 26, 10, 16, 64, 0.1, 16, None, None, 0, None))
+    assert st == md.MD_ERR_UNSUPPORTED and "130" in msg               # g*T = 13*10 rows
+    c64 = _cache(d=64)
+    st, msg = _err(lib.md_verify_attn_full(ctypes.byref(c64), 16, 26, 5, 16, 64, 0.1, 16, None, None, 0, None))
+    assert st == md.MD_ERR_UNSUPPORTED and "65" in msg                # head_dim 64: <= 64 rows
     c = _cache(stride_s=132)
     st, msg = _err(lib.md_draft_attn_sparse(ctypes.byref(c), 16, 4, 16, 4, 60, 0.1, 16, None, None, 0, None))
     assert st == md.MD_ERR_INVALID_ARG and "stride" in msg
@@ -152,3 +161,12 @@ def test_host_side_validation_of_selection_and_tp_calls():
                                                       None, 0, None))
     assert st == md.MD_ERR_INVALID_ARG
     assert md.pq_workspace_bytes(2, 2, 1000) > 0 and md.pq_workspace_bytes(0, 2, 1000) == 0
+
+
+def test_library_reads_no_environment():
+    """The product library has no hidden run-time knobs: no getenv in its sources (plan choices
+    are compile-time constants or functions of the call's arguments)."""
+    import glob
+    for path in glob.glob(os.path.join(ROOT, "paper_2408_11049_b200", "csrc", "*")):
+        src = open(path).read()
+        assert "getenv" not in src, path

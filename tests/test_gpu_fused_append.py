@@ -201,6 +201,7 @@ def test_fused_calls_in_a_cuda_graph():
     (2, 28, 4, 128, [5000, 4100], [2017, 2017], 2020, 32),
     (4, 8, 8, 64, [300, 200, 150, 90], [61, 64, 65, 3], 68, 7),
     (2, 4, 1, 128, [9000, 40], [1000, 8], 1000, 1),           # the tail is the new row alone
+    (3, 32, 8, 128, [3000, 700, 64], [100, 700, 64], 704, 0),  # no tail: the new row is a LISTED row
 ])
 def test_indexed_draft_append_parity(B, Hq, Hkv, d, lens, counts, stride, win):
     """md_draft_attn_indexed_append (SnapKV drafting, f2) = kv_append(kv_len - 1) + the indexed draft."""
@@ -212,7 +213,11 @@ def test_indexed_draft_append_parity(B, Hq, Hkv, d, lens, counts, stride, win):
     idx = np.full((B, Hkv, stride), -1, np.int32)
     for b in range(B):
         for h in range(Hkv):
-            idx[b, h, :counts[b]] = np.sort(rng.choice(int(tails[b]), size=int(counts[b]), replace=False))
+            if win == 0:  # tail_start = kv_len: list the new row n - 1 itself (PQ select with window 0)
+                pick = rng.choice(int(tails[b]) - 1, size=int(counts[b]) - 1, replace=False)
+                idx[b, h, :counts[b]] = np.sort(np.append(pick, tails[b] - 1))
+            else:
+                idx[b, h, :counts[b]] = np.sort(rng.choice(int(tails[b]), size=int(counts[b]), replace=False))
     kn, vn = _new_rows(B + 9, B, 1, Hkv, d)
     out = torch.full((B, Hq, d), float("nan"), device="cuda")
     lse = torch.full((B, Hq), float("nan"), device="cuda")

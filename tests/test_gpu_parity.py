@@ -69,6 +69,11 @@ VERIFY_CASES = [
     ("tc_generic_24",  2, 16, 4, 128, 6, [2000, 133]),       # tcgen05 kernel, NP=32, runtime R=24
     ("tc_generic_40",  2, 16, 2, 128, 5, [1500, 700]),       # tcgen05 kernel, NP=48, runtime R=40
     ("tc_np16_16",     2, 8, 2, 128, 4, [900, 260]),         # tcgen05 kernel, NP=16, R=16
+    # R > 48: the tcgen05 kernel's row groups (NG = NP / 32 groups of 32 rows, SURVEY §8(b) g*T <= 128)
+    ("tc_np64_56",     2, 28, 4, 128, 8, [3000, 190]),       # Qwen2.5 g=7, gamma=7: NP=64, 2 groups
+    ("tc_np96_77",     2, 28, 4, 128, 11, [2500, 133]),      # Qwen2.5, gamma=10: NP=96, 3 groups
+    ("tc_np128_112",   3, 28, 4, 128, 16, [2100, 300, 16]),  # Qwen2.5, gamma=15: NP=128, n = T edge
+    ("tc_np128_128",   2, 32, 4, 128, 16, [1800, 1000]),     # g=8 x T=16 = 128 rows, the ABI maximum
 ]
 
 
@@ -375,12 +380,13 @@ def test_large_batch_uses_global_walk():
     _cmp(o, l, ro, rl)
 
 
-def test_verify_rising_scores_exercise_max_raises():
+@pytest.mark.parametrize("Hq,Hkv,T", [(32, 8, 5), (28, 4, 16), (16, 2, 8)])
+def test_verify_rising_scores_exercise_max_raises(Hq, Hkv, T):
     """Scores that climb by ~4 (log2 units) every 128 keys force the tcgen05 kernel's lazy
     max raise (threshold 2^8) again and again inside a segment, so the thread-local row sums
     and the O^T accumulator in TMEM are rescaled many times; also a falling sequence (the max
     is set by the first stage and never raised)."""
-    B, Hq, Hkv, d, T = 2, 32, 8, 128, 5
+    B, d = 2, 128
     lens = [1500, 1100]
     case = AttnCase(B, Hq, Hkv, d, max(lens) + 8, lens, T=T, seed=97)
     one = S.k_to_bf16_bits(np.array([32]))[0]              # 1.0

@@ -149,16 +149,3 @@ def test_snapkv_select_per_sequence_budgets():
                                                 budgets=np.array(budgets))
     assert cnt.cpu().tolist() == ref_cnt.tolist() == [100 - w, 0, budget - w, budget - w]
     _check_selection(idx.cpu().numpy(), cnt.cpu().numpy(), ref_idx, ref_cnt, pooled)
-
-
-def test_snapkv_select_mma_sync_path():
-    """The mma.sync passes (MD_SNAP_TC=0; also every head_dim-64 call) on the d=128 cases."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, MD_SNAP_TC="0")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
-                        os.path.join(root, "tests", "test_gpu_snapkv.py"), "-k", "matches_oracle"],
-                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

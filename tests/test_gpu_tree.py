@@ -55,6 +55,8 @@ TREE_CASES = [
     ("keys_g2_d64",     2,  8,  4,  64, 4, [129, 90], "star"),
     ("qwen_rows",       2, 28,  4, 128, 2, [400, 100], "random"),
     ("rows_t16",        2,  4,  4, 128, 16, [260, 77], "random"),
+    ("tc_groups_t12",   2, 28,  4, 128, 12, [900, 140], "random"),  # 84 rows: tcgen05 row groups
+    ("tc_groups_t16",   2, 32,  4, 128, 16, [700, 20], "star"),     # 128 rows
 ]
 
 
