@@ -31,13 +31,15 @@ def bf16_to_f64(bits) -> np.ndarray:
 def softmax_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, scale: float):
     """The O2 core for one query row over an explicit key set.
 
-    q [d], k [n, d], v [n, d] (fp64) -> (o [d], lse).  Two passes: the maximum,
-    then exp-sum and the weighted sum, each summed in ascending key order."""
-    s = scale * (k @ q)                      # s_j = scale * q . k_j
+    q [d], k [n, d], v [n, d] (fp64) -> (o [d], lse).  Two passes: the maximum, then the
+    exp-sum and the weighted sum.  Every sum is taken sequentially in ascending index order
+    (np.cumsum's last element: a left-to-right recurrence, not BLAS's blocked order): the dot
+    products over c (each product of two bf16 values is exact in fp64), Z over j, o over j."""
+    s = scale * np.cumsum(k * q[None, :], axis=1)[:, -1]   # s_j = scale * sum_c q_c k_jc, c ascending
     m = s.max()
     w = np.exp(s - m)
-    z = w.sum()
-    o = (w @ v) / z
+    z = np.cumsum(w)[-1]                                   # Z = sum_j w_j, j ascending
+    o = np.cumsum(w[:, None] * v, axis=0)[-1] / z          # o = sum_j w_j v_j / Z, j ascending
     return o, m + np.log(z)
 
 

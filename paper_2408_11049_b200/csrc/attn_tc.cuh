@@ -35,24 +35,29 @@ constexpr int SMEM_MAX = 232448;             // 227 KB per CTA
 
 // NP = R rounded up to 16 query-row columns (<= 128: S^T x2 + O^T x2 = 4 NP <= 512 TMEM columns).
 // Up to 48 columns one group of 128 softmax threads holds every row's state in registers; above
-// that the rows are cut into NG groups of CW = 32 columns, each group a further 4 warps over the
-// same 128 TMEM lanes (warp w reads lane quadrant w % 4), so the per-thread state stays at 32 rows.
+// that the rows are cut into NG = 2 groups of CW = NP / 2 columns, each group a further 4 warps
+// over the same 128 TMEM lanes (warp w reads lane quadrant w % 4), which walk their columns in
+// chunks of CH = 32 (or 16) in two passes per stage (max test, then exponentials), so a thread
+// keeps only its CW row sums and one chunk of scores.
 template <int NP>
 struct Cfg {
-  static constexpr int NG = NP <= 48 ? 1 : NP / 32;  // row groups
+  static constexpr int NG = NP <= 48 ? 1 : 2;        // row groups
   static constexpr int CW = NP / NG;                 // query-row columns per group
+  static constexpr int CH = CW % 32 == 0 ? 32 : 16;  // columns per TMEM load chunk (NG > 1)
   static constexpr int SM_THREADS = 128 * NG;        // softmax / epilogue threads
   static constexpr int THREADS = SM_THREADS + 64;    // + producer warp + MMA warp
   static constexpr int NQ = NP <= 32 ? 2 : 1;        // Q buffers (by segment parity)
   static constexpr int QBUF = 2 * NP * 128;          // Q rows, two 64-column SW128 slabs
   static constexpr int PBUF = NP * KT * 2;           // P^T, 8x8 core matrices
-  static constexpr int AUX = 1024 + 6 * NP * 4;      // barriers, tmem slot, flags, plan; red[4NG][CW], mrow, crow
-  static constexpr int FIXED = NQ * QBUF + PBUF + AUX + TABLE_BYTES + 1024;
+  static constexpr int HDR = 384;                    // barriers, tmem slot, flags, plan
+  static constexpr int AUX = HDR + 6 * NP * 4;       // + red[4NG][CW], mrow[NP], crow[NP]
+  // the dynamic shared memory starts 1 KB aligned (no static __shared__; checked at entry)
+  static constexpr int FIXED = NQ * QBUF + PBUF + AUX + TABLE_BYTES;
   static constexpr int NSTAGE = (3 * STAGE + FIXED <= SMEM_MAX) ? 3 : 2;
   static constexpr int SMEM = NSTAGE * STAGE + FIXED;
   static constexpr int TMEM_COLS = 4 * NP <= 128 ? 128 : (4 * NP <= 256 ? 256 : 512);
   static_assert(NP % 16 == 0 && NP >= 16 && NP <= 128, "16 <= NP <= 128, a multiple of 16");
-  static_assert(NG == 1 || CW == 32, "groups of 32 columns");
+  static_assert(NG == 1 || CW % 16 == 0, "group columns in whole 16-column loads");
   static_assert(SMEM <= SMEM_MAX, "shared memory budget");
 };
 
@@ -186,8 +191,11 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
   const int R = RR > 0 ? RR : p.R;
   constexpr int NSTAGE = C::NSTAGE, NQ = C::NQ;
   constexpr int D = 128;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // SWIZZLE_128B tiles need 1 KB alignment: the dynamic window follows the 1 KB reserved block
+  // (no static shared memory), so it is aligned; the budget keeps no slack for realignment
+  if (smem_u32(smem_raw) & 1023u) __trap();
+  uint8_t* smem = smem_raw;
   uint8_t* ring = smem;
   uint8_t* qbuf = ring + NSTAGE * STAGE;
   uint8_t* pbuf = qbuf + NQ * C::QBUF;
@@ -207,7 +215,8 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(apb + 1);
   int* flag = reinterpret_cast<int*>(tslot + 4);                 // [16] finish_unit
   Plan* plan_smem = reinterpret_cast<Plan*>(flag + 16);          // 40 bytes (reserved 64)
-  float* red = reinterpret_cast<float*>(smem + NSTAGE * STAGE + NQ * C::QBUF + C::PBUF + 1024);  // [4NG][CW]
+  static_assert((4 * NSTAGE + 15) * 8 + 16 + 64 + 64 <= C::HDR, "barrier / flag header");
+  float* red = reinterpret_cast<float*>(smem + NSTAGE * STAGE + NQ * C::QBUF + C::PBUF + C::HDR);  // [4NG][CW]
   float* mrow = red + 4 * NP;                                    // [NP] running row maxima (log2 units)
   float* crow = mrow + NP;                                       // [NP] rescale factors / row sums
   int* pre = reinterpret_cast<int*>(crow + NP);                  // [TABLE_B + 1]
@@ -546,7 +555,8 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
       trace_put(p, 6, globaltimer());  // softmax end (ns): the CTA's finish time
     }
   } else if (active) {
-    // ============ softmax + epilogue, row group g of NG (CW = 32 columns [cb, cb + CW)) ============
+    // ===== softmax + epilogue, row group grp of NG = 2 (CW columns [cb, cb + CW), chunks of CH) =====
+    constexpr int CH = C::CH, NCH = CW / CH;
     const int x = threadIdx.x & 127;                // TMEM lane: key of the tile / head-dim row of O^T
     const int grp = threadIdx.x >> 7, wq = warp & 3, cb = grp * CW;
     const int bar_id = 2 + grp;                     // the group's named barrier
@@ -554,6 +564,11 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     float* gred = red + grp * 4 * CW;               // [4][CW] per-warp row partials of this group
     int it = 0, tt = 0, si = 0;
     float lacc[CW];
+    auto tload = [&](uint32_t addr, float* v) {     // CH consecutive TMEM columns
+#pragma unroll
+      for (int c = 0; c < CH; c += 16) tld16(addr + c, v + c);
+      wait_ld();
+    };
     while (walk.next(p, pre, sg)) {
       const int b = sg.b, kvh = sg.kvh, n = sg.n;
       const Ranges rg = seg_ranges(p, sg);
@@ -573,15 +588,18 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
         const int rel = pos + x - vbase;
         const float sl2 = p.scale_log2;
         const uint32_t s_col = tbase + sb * NP + cb + lane_off;
-        // hidden(r): key x is invisible to query row cb + r (past the valid keys, or a new key
-        // outside the row's causal chain / tree mask); only an edge stage hides anything
-        uint32_t hid = 0;  // bit r set: hidden
+        // dead(r): key x is invisible to query row cb + r (a padded row, a key past the valid
+        // range, or a new key outside the row's causal chain / tree mask)
+        uint64_t dead = 0;
+#pragma unroll
+        for (int r = 0; r < CW; ++r)
+          if (cb + r >= R) dead |= 1ull << r;
         if (edge) {
           int t = cb / p.g, hh = cb - t * p.g;
           uint32_t msk = t < p.T ? (p.tree_mask ? __ldg(p.tree_mask + (size_t)b * p.T + t) : ((2u << t) - 1u)) : 0u;
 #pragma unroll
           for (int r = 0; r < CW; ++r) {
-            if (!valid || (rel >= 0 && !((msk >> (rel & 31)) & 1u))) hid |= 1u << r;
+            if (!valid || (rel >= 0 && !((msk >> (rel & 31)) & 1u))) dead |= 1ull << r;
             if (++hh == p.g) {
               hh = 0;
               ++t;
@@ -591,38 +609,38 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
         }
         twait(&sfull[sb], (tt >> 1) & 1, nullptr);
         fence_after();
-        float xs[CW];
-        tld16(s_col, xs);
-        tld16(s_col + 16, xs + 16);
-        wait_ld();
+        // pass 1: does any score exceed its row maximum by > 2^8 (or meet m = -inf)?
         float xmax = -INFINITY;
 #pragma unroll
-        for (int r = 0; r < CW; r += 4) {
-          const float4 m4 = *reinterpret_cast<const float4*>(mrow + cb + r);
-          const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+        for (int ch = 0; ch < NCH; ++ch) {
+          float v[CH];
+          tload(s_col + ch * CH, v);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const bool live = (cb + r + i < R) && !((hid >> (r + i)) & 1u);
-            xs[r + i] = live ? fmaf(xs[r + i], sl2, -mm[i]) : -INFINITY;
-            xmax = fmaxf(xmax, xs[r + i]);
+          for (int r = 0; r < CH; r += 4) {
+            const float4 m4 = *reinterpret_cast<const float4*>(mrow + cb + ch * CH + r);
+            const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const bool live = !((dead >> (ch * CH + r + i)) & 1ull);
+              xmax = fmaxf(xmax, live ? fmaf(v[r + i], sl2, -mm[i]) : -INFINITY);
+            }
           }
         }
-        const bool need = xmax > THR;  // a score exceeds its row maximum by > 2^8 (or m = -inf)
         if (tt > 0) twait(pempty, (tt - 1) & 1, nullptr);  // previous PV done: P and O^T are free
-        if (vote_any128(need, bar_id)) {
-          // the scores are still in S^T (this group has not released the buffer): reload them
-          float v[CW];
-          tld16(s_col, v);
-          tld16(s_col + 16, v + 16);
-          wait_ld();
+        if (vote_any128(xmax > THR, bar_id)) {
+          // raise the group's row maxima to this tile's: per-row max over the 128 keys
 #pragma unroll
-          for (int r = 0; r < CW; ++r) {
-            const bool live = (cb + r < R) && !((hid >> r) & 1u);
-            v[r] = live ? v[r] * sl2 : -INFINITY;  // scaled score (log2 units)
-            float m = v[r];
+          for (int ch = 0; ch < NCH; ++ch) {
+            float v[CH];
+            tload(s_col + ch * CH, v);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-            if (lane == 0) gred[wq * CW + r] = m;
+            for (int i = 0; i < CH; ++i) {
+              const int r = ch * CH + i;
+              float m = ((dead >> r) & 1ull) ? -INFINITY : v[i] * sl2;
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+              if (lane == 0) gred[wq * CW + r] = m;
+            }
           }
           bar128(bar_id);
           if (x < CW) {
@@ -634,11 +652,7 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
           }
           bar128(bar_id);
 #pragma unroll
-          for (int r = 0; r < CW; ++r) {
-            const float mn = mrow[cb + r];
-            lacc[r] *= crow[cb + r];
-            xs[r] = (v[r] == -INFINITY) ? -INFINITY : v[r] - ((mn == -INFINITY) ? 0.f : mn);
-          }
+          for (int r = 0; r < CW; ++r) lacc[r] *= crow[cb + r];
           if (j > 0) {  // O^T already holds PV of earlier tiles of this segment: rescale it
             const uint32_t oa = tbase + 2 * NP + ob * NP + cb + lane_off;
 #pragma unroll
@@ -653,22 +667,36 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
             wait_st();
           }
         }
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sempty[sb]);  // S^T buffer sb is free (also after a reload)
-        // P = 2^x for the group's rows; row sums in fp32, the MMA operand is bf16
-        uint32_t pk[CW / 2];
-#pragma unroll
-        for (int r = 0; r < CW; r += 2) {
-          const float p0 = ex2(xs[r]), p1 = ex2(xs[r + 1]);  // ex2(-inf) = 0 for hidden / padded rows
-          lacc[r] += p0;
-          lacc[r + 1] += p1;
-          pk[r / 2] = pack_bf16(p0, p1);
-        }
+        // pass 2: P = 2^(s * scale * log2 e - m) for the group's rows; row sums in fp32, the MMA
+        // operand is bf16 (P^T core layout: key x -> core column x / 8, row (x % 8) * 16 B)
         uint8_t* pd = pbuf + (x >> 3) * 128 + (x & 7) * 16 + (cb / 8) * 2048;
 #pragma unroll
-        for (int c = 0; c < CW / 8; ++c)
-          *reinterpret_cast<uint4*>(pd + c * 2048) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        for (int ch = 0; ch < NCH; ++ch) {
+          float v[CH];
+          tload(s_col + ch * CH, v);
+          uint32_t pk[CH / 2];
+#pragma unroll
+          for (int r = 0; r < CH; r += 4) {
+            const float4 m4 = *reinterpret_cast<const float4*>(mrow + cb + ch * CH + r);
+            const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+            float pr[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const bool live = !((dead >> (ch * CH + r + i)) & 1ull);
+              pr[i] = live ? ex2(fmaf(v[r + i], sl2, -mm[i])) : 0.f;
+              lacc[ch * CH + r + i] += pr[i];
+            }
+            pk[r / 2] = pack_bf16(pr[0], pr[1]);
+            pk[r / 2 + 1] = pack_bf16(pr[2], pr[3]);
+          }
+#pragma unroll
+          for (int c = 0; c < CH / 8; ++c)
+            *reinterpret_cast<uint4*>(pd + (ch * CH / 8 + c) * 2048) =
+                make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[sb]);  // S^T buffer sb is read for the last time
         if (!valid && grp == 0) {  // zero this key's V row once (after the V half's TMA writes land)
           mbar_wait(&vfull[stage], (it / NSTAGE) & 1);
           zero_vrow(ring + stage * STAGE + 2 * SLAB + x * 128, x);
@@ -688,28 +716,29 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
       }
       bar128(bar_id);
       if (x < CW) crow[cb + x] = gred[x] + gred[CW + x] + gred[2 * CW + x] + gred[3 * CW + x];  // L_r
+      bar128(bar_id);
       mbar_wait(&ofull[ob], (si >> 1) & 1);
       fence_after();
-      float o[CW];
-      tld16(tbase + 2 * NP + ob * NP + cb + lane_off, o);
-      tld16(tbase + 2 * NP + ob * NP + cb + 16 + lane_off, o + 16);
-      wait_ld();
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&oempty[ob]);
-      bar128(bar_id);
       const bool complete = sg.complete();
       const int slot_base = chunk * 2 + pl.slot(sg.ustart, chunk);
 #pragma unroll
-      for (int r = 0; r < CW; ++r) {
-        const int row = cb + r;
-        if (row < R) {
-          const float L = crow[row];
-          const float val = (L > 0.f) ? o[r] / L : 0.f;
-          if (complete) store_out(p, o_row(p, b, kvh, row) * D + x, val);
-          else __stcg(p.ws_o + ((int64_t)slot_base * p.R + row) * D + x, val);
+      for (int ch = 0; ch < NCH; ++ch) {
+        float o[CH];
+        tload(tbase + 2 * NP + ob * NP + cb + ch * CH + lane_off, o);
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          const int row = cb + ch * CH + i;
+          if (row < R) {
+            const float L = crow[row];
+            const float val = (L > 0.f) ? o[i] / L : 0.f;
+            if (complete) store_out(p, o_row(p, b, kvh, row) * D + x, val);
+            else __stcg(p.ws_o + ((int64_t)slot_base * p.R + row) * D + x, val);
+          }
         }
       }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&oempty[ob]);
       if (x < CW && cb + x < R) {
         const float L = crow[cb + x], m = mrow[cb + x];
         const float lse2 = (L > 0.f) ? m + __log2f(L) : -INFINITY;

@@ -163,3 +163,102 @@ def test_synth_codebook_selects_needles():
                    if S._is_boosted_pos(9, 0, u, np.array([j]), Hkv, reg)[0]]
         assert 0 < len(boosted) <= 64
         assert set(boosted) <= set(idx[0, u, :cnt[0]].tolist())
+
+
+# ------------------------------------------------------------ off-grid: fp64 plain definition
+# On arbitrary bf16 inputs (Gaussian keys, queries and centroids, not on the k/32 grid) fp32
+# rounding does occur.  These pins bound the oracle's fixed-point pipeline (P1-P5, readings
+# Z26 / Z28) against the PLAIN fp64 product-quantisation definition: nearest centroid by the
+# exact squared distance, the PQ inner product sum_hh q_hh . khat_j in fp64, exact top-k of it.
+# A deviation is allowed only where fp32 rounding can decide it: a near-tie within an error
+# bound derived from the arithmetic (n-term fp32 sums: |err| <= n 2^-24 sum |terms|).
+U = 2.0 ** -24
+
+
+def _offgrid_bits(rng, shape, sigma=1.0):
+    x = (rng.standard_normal(shape) * sigma).astype(np.float32)
+    b = x.view(np.uint32)
+    return ((b + 0x7FFF + ((b >> 16) & 1)) >> 16).astype(np.uint16)     # round to nearest bf16
+
+
+def test_offgrid_encode_is_fp64_nearest_centroid_up_to_rounding_ties():
+    rng = np.random.default_rng(21)
+    for d in (64, 128):
+        s = d // 16
+        k = _offgrid_bits(rng, (2000, d))
+        cb = _offgrid_bits(rng, (16, 256, s))
+        codes = PQ.pq_encode(k, cb)
+        x, C = _f64(k), _f64(cb)
+        ndiff = 0
+        for m in range(16):
+            diff = x[:, None, m * s:(m + 1) * s] - C[m][None]          # [n, 256, s], exact in fp64
+            dist = (diff ** 2).sum(-1)
+            best = np.argmin(dist, axis=1)
+            # fp32 left-to-right sum of s squares: |err| <= (s + 2) 2^-24 * dist (sub, mul, adds)
+            bound = (s + 2) * U * dist
+            rows = np.nonzero(codes[:, m] != best)[0]
+            ndiff += len(rows)
+            for j in rows:
+                c32, c64 = int(codes[j, m]), int(best[j])
+                assert dist[j, c32] - dist[j, c64] <= bound[j, c32] + bound[j, c64], (d, m, j)
+        assert ndiff <= 2000 * 16 * 1e-3      # near-ties are rare
+
+
+def test_offgrid_scores_are_the_pq_inner_product_within_the_rounding_bound():
+    rng = np.random.default_rng(22)
+    for d, g in ((128, 4), (128, 7), (64, 1)):
+        s = d // 16
+        q = _offgrid_bits(rng, (g, d))
+        cb = _offgrid_bits(rng, (16, 256, s))
+        codes = rng.integers(0, 256, size=(3000, 16)).astype(np.uint8)
+        lut = PQ.pq_lut(q, cb)
+        e = PQ.lut_exponent(lut)
+        sc = PQ.pq_scores(PQ.pq_lut_fixed(lut), codes).astype(np.float64) * 2.0 ** -e
+        Q, C = _f64(q), _f64(cb)
+        khat = np.concatenate([C[m][codes[:, m]] for m in range(16)], axis=1)      # [n, d]
+        exact = khat @ Q.sum(0)                                                     # fp64 PQ score
+        # per table entry: g*s products and sums in fp32 -> <= 2 g s 2^-24 sum |q c|; then rint
+        # to the 2^-e grid: <= 2^-e / 2 per entry; 16 entries per score
+        absterm = np.stack([np.abs(C[m]) @ np.abs(Q[:, m * s:(m + 1) * s]).sum(0) for m in range(16)])  # [16, 256]
+        ent_bound = 2 * g * s * U * absterm + 0.5 * 2.0 ** -e
+        bound = sum(ent_bound[m][codes[:, m]] for m in range(16))
+        err = np.abs(sc - exact)
+        assert np.all(err <= bound), float(np.max(err / bound))
+        assert np.max(err) > 0          # off-grid: rounding really happens (the bound is exercised)
+
+
+def test_offgrid_selection_is_exact_pq_topk_up_to_near_ties():
+    """P5 on the oracle's fixed-point scores vs exact top-k of the fp64 PQ scores: identical sets
+    except positions whose fp64 score ties the k-th largest within twice the score bound."""
+    rng = np.random.default_rng(23)
+    B, Hkv, g, d, n = 2, 2, 4, 128, 1500
+    s = d // 16
+    sink, window, budget = 4, 64, 200
+    k = _offgrid_bits(rng, (B, Hkv, n, d))
+    q = _offgrid_bits(rng, (B, Hkv * g, d))
+    cb = _offgrid_bits(rng, (B, Hkv, 16, 256, s))
+    codes = PQ.pq_encode_cache(k, cb, np.zeros(B, np.int64), n)
+    kv_len = np.array([n, n - 333], dtype=np.int32)
+    idx, cnt, tail, _ = PQ.pq_select(q, cb, codes, kv_len, sink, window, budget)
+    ndiff = 0
+    for b in range(B):
+        nb = int(kv_len[b])
+        s0, t0, c = PQ.select_window(nb, sink, window, budget)
+        for u in range(Hkv):
+            Q, C = _f64(q[b, u * g:(u + 1) * g]), _f64(cb[b, u])
+            khat = np.concatenate([C[m][codes[b, u, :nb, m]] for m in range(16)], axis=1)
+            exact = khat @ Q.sum(0)
+            lut = PQ.pq_lut(q[b, u * g:(u + 1) * g], cb[b, u])
+            e = PQ.lut_exponent(lut)
+            absterm = np.stack([np.abs(C[m]) @ np.abs(Q[:, m * s:(m + 1) * s]).sum(0) for m in range(16)])
+            ent = 2 * g * s * U * absterm + 0.5 * 2.0 ** -e
+            bound = sum(ent[m][codes[b, u, :nb, m]] for m in range(16))
+            cand = np.arange(s0, t0)
+            ref = set(sorted(cand, key=lambda j: (-exact[j], j))[:c])
+            got = idx[b, u, s0:s0 + c].tolist()
+            assert idx[b, u, :s0].tolist() == list(range(s0))
+            thr = np.sort(exact[s0:t0])[::-1][c - 1]
+            for x in ref ^ set(got):
+                ndiff += 1
+                assert abs(exact[x] - thr) <= 2 * bound.max(), (b, u, x)
+    assert ndiff <= 4
