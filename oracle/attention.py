@@ -28,18 +28,20 @@ def bf16_to_f64(bits) -> np.ndarray:
     return b.view(np.float32).astype(np.float64)
 
 
-def softmax_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, scale: float):
+def softmax_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, scale: float, vT=None):
     """The O2 core for one query row over an explicit key set.
 
     q [d], k [n, d], v [n, d] (fp64) -> (o [d], lse).  Two passes: the maximum, then the
     exp-sum and the weighted sum.  Every sum is taken sequentially in ascending index order
     (np.cumsum's last element: a left-to-right recurrence, not BLAS's blocked order): the dot
-    products over c (each product of two bf16 values is exact in fp64), Z over j, o over j."""
+    products over c (each product of two bf16 values is exact in fp64), Z over j, o over j.
+    vT: optionally v transposed ([d, n], any strides; only a faster memory layout, same sums)."""
     s = scale * np.cumsum(k * q[None, :], axis=1)[:, -1]   # s_j = scale * sum_c q_c k_jc, c ascending
     m = s.max()
     w = np.exp(s - m)
     z = np.cumsum(w)[-1]                                   # Z = sum_j w_j, j ascending
-    o = np.cumsum(w[:, None] * v, axis=0)[-1] / z          # o = sum_j w_j v_j / Z, j ascending
+    vT = v.T if vT is None else vT
+    o = np.cumsum(vT * w[None, :], axis=1)[:, -1] / z      # o_c = sum_j w_j v_jc / Z, j ascending
     return o, m + np.log(z)
 
 
@@ -57,10 +59,12 @@ def verify_attn_full(q_bits, k_cache_bits, v_cache_bits, kv_len, scale):
         for kvh in range(Hkv):
             K = bf16_to_f64(k_cache_bits[b, kvh, :n])
             V = bf16_to_f64(v_cache_bits[b, kvh, :n])
+            VT = np.ascontiguousarray(V.T)
             for t in range(T):
                 last = n - T + t                  # row t sees keys [0, n - T + t]
                 for h in range(kvh * g, (kvh + 1) * g):
-                    out[b, t, h], lse[b, t, h] = softmax_attention(q[b, t, h], K[: last + 1], V[: last + 1], scale)
+                    out[b, t, h], lse[b, t, h] = softmax_attention(q[b, t, h], K[: last + 1], V[: last + 1], scale,
+                                                                   VT[:, : last + 1])
     return out, lse
 
 

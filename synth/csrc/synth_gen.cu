@@ -31,9 +31,11 @@ __device__ __forceinline__ uint16_t bf16_of_k(int k) {
   return (uint16_t)(__float_as_uint(f) >> 16);
 }
 
+// (b0, h0, Htot): the tensor is the slice [b0, b0 + B) x [h0, h0 + Hkv) of a cache with Htot KV
+// heads, so a tensor-parallel / batch shard holds exactly the values of the full cache's slice
 __global__ void fill_cache_kernel(uint16_t* base, int B, int Hkv, int d, long long sB, long long sH, long long sS,
                                   int pos0, int npos, uint64_t key, uint64_t key_dir, uint64_t key_needle,
-                                  int peaky, int sink, int a_k, int needle_period) {
+                                  int peaky, int sink, int a_k, int needle_period, int b0, int h0, int Htot) {
   const long long total = (long long)B * Hkv * npos * d;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -44,7 +46,7 @@ __global__ void fill_cache_kernel(uint16_t* base, int B, int Hkv, int d, long lo
     const int h = (int)(r % Hkv);
     const int b = (int)(r / Hkv);
     const uint64_t pos = (uint64_t)(pos0 + pl);
-    const uint64_t unit = (uint64_t)b * Hkv + h;
+    const uint64_t unit = (uint64_t)(b0 + b) * Htot + (h0 + h);
     int k = grid_k(key, (unit * POSMAX + pos) * d + c);
     if (peaky) {
       const bool needle = (mix64(unit * POSMAX + pos + key_needle) % (uint64_t)needle_period) == 0;
@@ -83,15 +85,23 @@ unsigned grid_for(long long total) {
 
 }  // namespace
 
-extern "C" __attribute__((visibility("default"))) int mds_fill_cache(void* base, int B, int Hkv, int d, long long sB, long long sH, long long sS, int pos0,
-                              int npos, unsigned long long seed, int tensor, int peaky, int sink, int a_k,
-                              int needle_period, void* stream) {
+extern "C" __attribute__((visibility("default"))) int mds_fill_cache_slice(
+    void* base, int B, int Hkv, int d, long long sB, long long sH, long long sS, int pos0, int npos,
+    unsigned long long seed, int tensor, int peaky, int sink, int a_k, int needle_period, int b0, int h0, int Htot,
+    void* stream) {
   const long long total = (long long)B * Hkv * npos * d;
   if (total <= 0) return 0;
   fill_cache_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(
       (uint16_t*)base, B, Hkv, d, sB, sH, sS, pos0, npos, key_of(seed, tensor), key_of(seed, T_DIR),
-      key_of(seed, T_NEEDLE), peaky && tensor == (int)T_KCACHE, sink, a_k, needle_period);
+      key_of(seed, T_NEEDLE), peaky && tensor == (int)T_KCACHE, sink, a_k, needle_period, b0, h0, Htot);
   return (int)cudaGetLastError();
+}
+
+extern "C" __attribute__((visibility("default"))) int mds_fill_cache(void* base, int B, int Hkv, int d, long long sB, long long sH, long long sS, int pos0,
+                              int npos, unsigned long long seed, int tensor, int peaky, int sink, int a_k,
+                              int needle_period, void* stream) {
+  return mds_fill_cache_slice(base, B, Hkv, d, sB, sH, sS, pos0, npos, seed, tensor, peaky, sink, a_k, needle_period,
+                              0, 0, Hkv, stream);
 }
 
 // Queries [B][T][Hq][d] (T = 1 for draft queries); also the new K/V rows [B][T][Hkv][d]

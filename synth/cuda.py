@@ -23,17 +23,23 @@ def _load():
         _lib.mds_fill_cache.argtypes = [ctypes.c_void_p, i, i, i, ll, ll, ll, i, i, ctypes.c_ulonglong, i, i, i, i,
                                         i, ctypes.c_void_p]
         _lib.mds_fill_q.argtypes = [ctypes.c_void_p, i, i, i, i, i, ctypes.c_ulonglong, i, i, i, ctypes.c_void_p]
+        _lib.mds_fill_cache_slice.argtypes = [ctypes.c_void_p, i, i, i, ll, ll, ll, i, i, ctypes.c_ulonglong, i, i, i,
+                                              i, i, i, i, i, ctypes.c_void_p]
     return _lib
 
 
-def fill_cache(x: torch.Tensor, seed: int, tensor: int, pos0: int, npos: int, regime: Regime = FLAT):
-    """x: [B, Hkv, cap, d] bf16 view; fills rows [pos0, pos0 + npos) like synth.kv_cache_k."""
+def fill_cache(x: torch.Tensor, seed: int, tensor: int, pos0: int, npos: int, regime: Regime = FLAT,
+               b0: int = 0, h0: int = 0, Hkv_total: int | None = None):
+    """x: [B, Hkv, cap, d] bf16 view; fills rows [pos0, pos0 + npos) like synth.kv_cache_k.
+    (b0, h0, Hkv_total): x is the slice [b0, b0 + B) x [h0, h0 + Hkv) of a cache with Hkv_total
+    KV heads (a tensor-parallel / batch shard gets exactly the full cache's values)."""
     B, H, cap, d = x.shape
     assert x.dtype == torch.bfloat16 and x.stride(3) == 1 and pos0 + npos <= cap
     s = torch.cuda.current_stream().cuda_stream
-    rc = _load().mds_fill_cache(x.data_ptr(), B, H, d, x.stride(0), x.stride(1), x.stride(2), pos0, npos, seed,
-                                tensor, int(regime.kind == "peaky" and tensor == T_KCACHE), regime.sink, regime.a_k,
-                                regime.needle_period, s)
+    rc = _load().mds_fill_cache_slice(x.data_ptr(), B, H, d, x.stride(0), x.stride(1), x.stride(2), pos0, npos, seed,
+                                      tensor, int(regime.kind == "peaky" and tensor == T_KCACHE), regime.sink,
+                                      regime.a_k, regime.needle_period, b0, h0, H if Hkv_total is None else Hkv_total,
+                                      s)
     if rc:
         raise RuntimeError(f"mds_fill_cache failed: {rc}")
 

@@ -39,3 +39,14 @@ def test_query_and_new_kv_generators_bit_exact(regime):
     kn = torch.empty((3, 5, 8, 128), dtype=torch.bfloat16, device="cuda")
     SC.fill_new_kv(kn, 4, S.T_KNEW)
     assert np.array_equal(_bits(kn), S.k_to_bf16_bits(S.new_kv_k(4, S.T_KNEW, 3, 5, 8, 128)))
+
+
+def test_cache_slice_generator_equals_the_full_cache_slice():
+    """A tensor-parallel / batch shard (b0, h0 of a cache with Hkv_total heads) holds exactly the
+    full cache's values, so sharded runs see the same inputs as the single-GPU run."""
+    reg = S.Regime("peaky", sink=4, needle_period=37)
+    B, H, cap, d = 4, 8, 200, 128
+    full = S.k_to_bf16_bits(S.kv_cache_k(13, S.T_KCACHE, B, H, d, 0, cap, regime=reg))
+    shard = torch.zeros((2, 2, cap, d), dtype=torch.bfloat16, device="cuda")
+    SC.fill_cache(shard, 13, S.T_KCACHE, 0, cap, reg, b0=2, h0=4, Hkv_total=H)
+    assert np.array_equal(_bits(shard), full[2:4, 4:6])
