@@ -160,6 +160,45 @@ def new_kv_k(seed: int, tensor: int, B: int, T: int, Hkv: int, d: int) -> np.nda
 
 
 # ----------------------------------------------------------------------------------------
+# off-grid values: arbitrary bf16 bit patterns (full 8-bit significand, 7 binades), |x| < 1
+# ----------------------------------------------------------------------------------------
+def offgrid_bits_from_hash(h: np.ndarray) -> np.ndarray:
+    """bf16 bits from a uint64 hash: sign, biased exponent 120..126 (|x| in [2^-7, 1)), and a
+    random 7-bit mantissa -- values OFF the k/32 grid (every bf16 in that range is reachable),
+    so fp32 rounding in QK^T and the softmax really happens; |x| < 1 keeps the north_star
+    tolerance derivation (bf16 P error <= 2^-9 max|v|) valid."""
+    h = np.asarray(h, dtype=U64)
+    sign = ((h >> U64(63)) & U64(1)).astype(np.uint16)
+    ex = (((h >> U64(40)) & U64(0xFFFF)) % U64(7)).astype(np.uint16) + np.uint16(120)
+    man = ((h >> U64(20)) & U64(0x7F)).astype(np.uint16)
+    return (sign << np.uint16(15)) | (ex << np.uint16(7)) | man
+
+
+def kv_cache_bits_offgrid(seed: int, tensor: int, B: int, Hkv: int, d: int, pos0: int, npos: int,
+                          b_sel=None, h_sel=None) -> np.ndarray:
+    """Off-grid cache rows pos0..pos0+npos-1 -> uint16 bf16 bits [nb, nh, npos, d] (the same
+    hash index as kv_cache_k)."""
+    bs = np.arange(B) if b_sel is None else np.asarray(b_sel)
+    hs = np.arange(Hkv) if h_sel is None else np.asarray(h_sel)
+    b = bs[:, None, None, None].astype(U64)
+    h = hs[None, :, None, None].astype(U64)
+    p = (np.arange(npos, dtype=np.int64) + pos0)[None, None, :, None]
+    c = np.arange(d, dtype=np.int64)[None, None, None, :]
+    idx = ((b * U64(Hkv) + h) * U64(POSMAX) + p.astype(U64)) * U64(d) + c.astype(U64)
+    return offgrid_bits_from_hash(hash_u64(seed, tensor, idx))
+
+
+def flat_bits_offgrid(seed: int, tensor: int, shape, b_sel=None) -> np.ndarray:
+    """Off-grid values of a contiguous tensor (queries [B, T, Hq, d], new rows [B, T, Hkv, d]),
+    element i hashed by its flat index; b_sel selects rows of the leading dimension."""
+    shape = tuple(shape)
+    per = int(np.prod(shape[1:]))
+    bs = np.arange(shape[0]) if b_sel is None else np.asarray(b_sel)
+    idx = (bs[:, None].astype(U64) * U64(per) + np.arange(per, dtype=np.int64)[None, :].astype(U64))
+    return offgrid_bits_from_hash(hash_u64(seed, tensor, idx)).reshape((len(bs),) + shape[1:])
+
+
+# ----------------------------------------------------------------------------------------
 # lengths
 # ----------------------------------------------------------------------------------------
 def committed_lengths(seed: int, B: int, ctx: int, gamma: int, ragged: bool) -> np.ndarray:

@@ -78,6 +78,37 @@ __global__ void fill_q_kernel(uint16_t* q, int B, int T, int Hq, int Hkv, int d,
   }
 }
 
+// off-grid bf16 bits (synth.offgrid_bits_from_hash): sign, exponent 120..126, 7-bit mantissa
+__device__ __forceinline__ uint16_t offgrid_bits(uint64_t h) {
+  const uint16_t sign = (uint16_t)((h >> 63) & 1u);
+  const uint16_t ex = (uint16_t)(((h >> 40) & 0xFFFFu) % 7u) + 120u;
+  const uint16_t man = (uint16_t)((h >> 20) & 0x7Fu);
+  return (uint16_t)((sign << 15) | (ex << 7) | man);
+}
+
+__global__ void fill_cache_offgrid_kernel(uint16_t* base, int B, int Hkv, int d, long long sB, long long sH,
+                                          long long sS, int pos0, int npos, uint64_t key, int b0, int h0, int Htot) {
+  const long long total = (long long)B * Hkv * npos * d;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % d);
+    long long r = i / d;
+    const int pl = (int)(r % npos);
+    r /= npos;
+    const int h = (int)(r % Hkv);
+    const int b = (int)(r / Hkv);
+    const uint64_t unit = (uint64_t)(b0 + b) * Htot + (h0 + h);
+    const uint64_t pos = (uint64_t)(pos0 + pl);
+    base[b * sB + h * sH + (long long)(pos0 + pl) * sS + c] = offgrid_bits(mix64((unit * POSMAX + pos) * d + c + key));
+  }
+}
+
+__global__ void fill_flat_offgrid_kernel(uint16_t* x, long long total, uint64_t key) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = offgrid_bits(mix64((uint64_t)i + key));
+}
+
 unsigned grid_for(long long total) {
   long long blocks = (total + 255) / 256;
   return (unsigned)(blocks > 65536 ? 65536 : (blocks < 1 ? 1 : blocks));
@@ -113,5 +144,25 @@ extern "C" __attribute__((visibility("default"))) int mds_fill_q(void* q, int B,
   fill_q_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>((uint16_t*)q, B, T, Hq, Hkv, d,
                                                                     key_of(seed, tensor), key_of(seed, T_DIR),
                                                                     peaky, a_q);
+  return (int)cudaGetLastError();
+}
+
+// off-grid twins of synth.kv_cache_bits_offgrid / synth.flat_bits_offgrid
+extern "C" __attribute__((visibility("default"))) int mds_fill_cache_offgrid(
+    void* base, int B, int Hkv, int d, long long sB, long long sH, long long sS, int pos0, int npos,
+    unsigned long long seed, int tensor, int b0, int h0, int Htot, void* stream) {
+  const long long total = (long long)B * Hkv * npos * d;
+  if (total <= 0) return 0;
+  fill_cache_offgrid_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(
+      (uint16_t*)base, B, Hkv, d, sB, sH, sS, pos0, npos, key_of(seed, tensor), b0, h0, Htot);
+  return (int)cudaGetLastError();
+}
+
+extern "C" __attribute__((visibility("default"))) int mds_fill_flat_offgrid(void* x, long long total,
+                                                                         unsigned long long seed, int tensor,
+                                                                         void* stream) {
+  if (total <= 0) return 0;
+  fill_flat_offgrid_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>((uint16_t*)x, total,
+                                                                              key_of(seed, tensor));
   return (int)cudaGetLastError();
 }

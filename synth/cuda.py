@@ -23,6 +23,9 @@ def _load():
         _lib.mds_fill_cache.argtypes = [ctypes.c_void_p, i, i, i, ll, ll, ll, i, i, ctypes.c_ulonglong, i, i, i, i,
                                         i, ctypes.c_void_p]
         _lib.mds_fill_q.argtypes = [ctypes.c_void_p, i, i, i, i, i, ctypes.c_ulonglong, i, i, i, ctypes.c_void_p]
+        _lib.mds_fill_cache_offgrid.argtypes = [ctypes.c_void_p, i, i, i, ll, ll, ll, i, i, ctypes.c_ulonglong, i, i,
+                                                i, i, ctypes.c_void_p]
+        _lib.mds_fill_flat_offgrid.argtypes = [ctypes.c_void_p, ll, ctypes.c_ulonglong, i, ctypes.c_void_p]
         _lib.mds_fill_cache_slice.argtypes = [ctypes.c_void_p, i, i, i, ll, ll, ll, i, i, ctypes.c_ulonglong, i, i, i,
                                               i, i, i, i, i, ctypes.c_void_p]
     return _lib
@@ -65,3 +68,23 @@ def fill_new_kv(x: torch.Tensor, seed: int, tensor: int):
     rc = _load().mds_fill_q(x.data_ptr(), B, T, H, H, d, seed, tensor, 0, 0, s)
     if rc:
         raise RuntimeError(f"mds_fill_q failed: {rc}")
+
+
+def fill_cache_offgrid(x: torch.Tensor, seed: int, tensor: int, pos0: int, npos: int, b0: int = 0, h0: int = 0,
+                       Hkv_total: int | None = None):
+    """Off-grid twin of synth.kv_cache_bits_offgrid for rows [pos0, pos0 + npos) of x [B, Hkv, cap, d]."""
+    B, H, cap, d = x.shape
+    assert x.dtype == torch.bfloat16 and x.stride(3) == 1 and pos0 + npos <= cap
+    rc = _load().mds_fill_cache_offgrid(x.data_ptr(), B, H, d, x.stride(0), x.stride(1), x.stride(2), pos0, npos,
+                                        seed, tensor, b0, h0, H if Hkv_total is None else Hkv_total,
+                                        torch.cuda.current_stream().cuda_stream)
+    if rc:
+        raise RuntimeError(f"mds_fill_cache_offgrid failed: {rc}")
+
+
+def fill_flat_offgrid(x: torch.Tensor, seed: int, tensor: int):
+    """Off-grid twin of synth.flat_bits_offgrid for a contiguous bf16 tensor."""
+    assert x.dtype == torch.bfloat16 and x.is_contiguous()
+    rc = _load().mds_fill_flat_offgrid(x.data_ptr(), x.numel(), seed, tensor, torch.cuda.current_stream().cuda_stream)
+    if rc:
+        raise RuntimeError(f"mds_fill_flat_offgrid failed: {rc}")

@@ -50,3 +50,17 @@ def test_cache_slice_generator_equals_the_full_cache_slice():
     shard = torch.zeros((2, 2, cap, d), dtype=torch.bfloat16, device="cuda")
     SC.fill_cache(shard, 13, S.T_KCACHE, 0, cap, reg, b0=2, h0=4, Hkv_total=H)
     assert np.array_equal(_bits(shard), full[2:4, 4:6])
+
+
+def test_offgrid_generators_bit_exact():
+    B, H, cap, d = 3, 4, 130, 128
+    k = torch.zeros((B, H, cap, d), dtype=torch.bfloat16, device="cuda")
+    SC.fill_cache_offgrid(k, 17, S.T_KCACHE, 0, cap)
+    assert np.array_equal(_bits(k), S.kv_cache_bits_offgrid(17, S.T_KCACHE, B, H, d, 0, cap))
+    shard = torch.zeros((1, 2, cap, d), dtype=torch.bfloat16, device="cuda")
+    SC.fill_cache_offgrid(shard, 17, S.T_KCACHE, 0, cap, b0=2, h0=1, Hkv_total=H)
+    assert np.array_equal(_bits(shard), S.kv_cache_bits_offgrid(17, S.T_KCACHE, B, H, d, 0, cap)[2:3, 1:3])
+    q = torch.zeros((3, 5, 32, 128), dtype=torch.bfloat16, device="cuda")
+    SC.fill_flat_offgrid(q, 17, S.T_QVERIFY)
+    assert np.array_equal(_bits(q), S.flat_bits_offgrid(17, S.T_QVERIFY, (3, 5, 32, 128)))
+    assert np.array_equal(_bits(q)[1:2], S.flat_bits_offgrid(17, S.T_QVERIFY, (3, 5, 32, 128), b_sel=[1]))

@@ -45,3 +45,15 @@ def test_spec_probs_rows_are_distributions_and_overlap_tracks_sigma():
     b1 = np.mean([S.overlap(p[b, j], q[b, j]) for b in range(2) for j in range(3)])
     b2 = np.mean([S.overlap(p2[b, j], q2[b, j]) for b in range(2) for j in range(3)])
     assert b1 > b2
+
+
+def test_offgrid_values_are_off_grid_and_bounded():
+    """Off-grid generator: every value is a finite bf16 with |x| in [2^-7, 1), most are not
+    multiples of 1/32 (so fp32 rounding happens in the attention), signs are balanced."""
+    bits = S.kv_cache_bits_offgrid(5, S.T_KCACHE, 2, 3, 128, 0, 200)
+    x = S.bf16_bits_to_f32(bits).astype(np.float64)
+    assert np.all(np.isfinite(x)) and np.all(np.abs(x) < 1.0) and np.all(np.abs(x) >= 2.0 ** -7)
+    assert np.mean(np.abs(x * 32 - np.round(x * 32)) > 0) > 0.5
+    assert abs(np.mean(np.sign(x))) < 0.05
+    q = S.flat_bits_offgrid(5, S.T_QVERIFY, (2, 5, 8, 64))
+    assert q.shape == (2, 5, 8, 64) and np.array_equal(q[1:], S.flat_bits_offgrid(5, S.T_QVERIFY, (2, 5, 8, 64), [1]))
