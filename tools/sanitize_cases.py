@@ -1,0 +1,73 @@
+"""Small launches of every attention-path kernel family for compute-sanitizer (racecheck /
+synccheck / memcheck): tcgen05 verify (one and two row groups, fused append, split units),
+the mma.sync keys kernel (draft, fused append, indexed draft), the rows kernel (head_dim 64),
+and the SnapKV tcgen05 scoring passes.  usage: python tools/sanitize_cases.py"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2408_11049_b200 as md  # noqa: E402
+import synth as S  # noqa: E402
+from tests.helpers import AttnCase, bits_to_torch_bf16  # noqa: E402
+
+
+def verify(case, T, fused=False):
+    B, Hq, d = case.B, case.Hq, case.d
+    out = torch.empty((B, T, Hq, d), device="cuda")
+    lse = torch.empty((B, T, Hq), device="cuda")
+    mkl = int(case.kv_len.max())
+    ws = torch.zeros(md.attn_workspace_bytes(B, Hq, case.Hkv, d, T, mkl), dtype=torch.uint8, device="cuda")
+    if fused:
+        kn = bits_to_torch_bf16(S.k_to_bf16_bits(S.new_kv_k(3, S.T_KNEW, B, T, case.Hkv, d)))
+        md.verify_attn_full_append(case.qv, case.k, case.v, kn, kn, case.kv_len_t, mkl, case.scale, out, lse, ws)
+    else:
+        md.verify_attn_full(case.qv, case.k, case.v, case.kv_len_t, mkl, case.scale, out, lse, ws)
+
+
+def draft(case, sink, window, fused=False):
+    B, Hq, d = case.B, case.Hq, case.d
+    out = torch.empty((B, Hq, d), device="cuda")
+    lse = torch.empty((B, Hq), device="cuda")
+    ws = torch.zeros(md.attn_workspace_bytes(B, Hq, case.Hkv, d, 1, sink + window), dtype=torch.uint8, device="cuda")
+    if fused:
+        kn = bits_to_torch_bf16(S.k_to_bf16_bits(S.new_kv_k(4, S.T_KNEW, B, 1, case.Hkv, d)))
+        md.draft_attn_sparse_append(case.qd, case.k, case.v, kn, kn, case.kv_len_t, sink, window, case.scale, out, lse,
+                                    ws)
+    else:
+        md.draft_attn_sparse(case.qd, case.k, case.v, case.kv_len_t, sink, window, case.scale, out, lse, ws)
+
+
+def main():
+    md.load_library()
+    which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if which in ("all", "tc"):
+        verify(AttnCase(2, 32, 8, 128, 2100, [2100, 700], T=5, seed=1).to_cuda(), 5)             # R = 20
+        verify(AttnCase(2, 32, 8, 128, 2100, [2100, 700], T=5, seed=1).to_cuda(), 5, fused=True)
+        verify(AttnCase(1, 4, 1, 128, 9000, [9000], T=5, seed=2).to_cuda(), 5)                   # split unit
+        verify(AttnCase(2, 28, 4, 128, 1500, [1500, 300], T=8, seed=3).to_cuda(), 8)             # R = 56: 2 groups
+        verify(AttnCase(2, 28, 4, 128, 900, [900, 20], T=16, seed=4).to_cuda(), 16)              # R = 112
+    if which in ("all", "keys"):
+        c = AttnCase(3, 32, 8, 128, 3000, [3000, 1030, 64], T=1, seed=5).to_cuda()
+        draft(c, 4, 1020)
+        draft(c, 4, 1020, fused=True)
+        verify(AttnCase(2, 32, 32, 128, 1200, [1200, 333], T=4, seed=6).to_cuda(), 4)            # MHA verify
+    if which in ("all", "rows"):
+        verify(AttnCase(2, 16, 2, 64, 800, [800, 129], T=8, seed=7).to_cuda(), 8)                # d = 64, R = 64
+    if which in ("all", "snap"):
+        B, Hq, Hkv, d, w, budget = 2, 32, 8, 128, 32, 256
+        L = [1500, 900]
+        case = AttnCase(B, Hq, Hkv, d, 1600, L, seed=8).to_cuda()
+        q_obs = bits_to_torch_bf16(S.k_to_bf16_bits(S.q_rows_k(8, S.T_QVERIFY, B, w, Hq, Hkv, d)))
+        idx = torch.zeros((B, Hkv, budget), dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(B, dtype=torch.int32, device="cuda")
+        md.snapkv_select(case.k, case.v, q_obs, torch.tensor(L, dtype=torch.int32).cuda(), max(L), w, budget,
+                         case.scale, idx, cnt)
+    torch.cuda.synchronize()
+    print("sanitize cases done:", which)
+
+
+if __name__ == "__main__":
+    main()
