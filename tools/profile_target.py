@@ -1,7 +1,8 @@
 """Run a few md_verify_attn_full / md_draft_attn_sparse calls of one bench config (for ncu).
 
-usage: python tools/profile_target.py [config] [n_calls] [fused]
-("fused": the md_*_append calls, with the new K/V rows written inside the kernel, as bench.py runs them)"""
+usage: python tools/profile_target.py [config] [n_calls] [fused|plain] [gamma]
+("fused": the md_*_append calls, with the new K/V rows written inside the kernel, as bench.py runs them;
+gamma: override the config's gamma, e.g. to profile the verify kernel's larger row counts)"""
 import os
 import sys
 
@@ -18,6 +19,8 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "llama3_b64_32k"
 ncalls = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 fused = len(sys.argv) > 3 and sys.argv[3] == "fused"
 B, Hq, Hkv, d, ctx, gamma, sink, window, V, layers, alpha = CONFIGS[cfg]
+if len(sys.argv) > 4:
+    gamma = int(sys.argv[4])
 T, R = gamma + 1, 2
 cap = ctx + 64
 reg = S.Regime("peaky", sink=sink)
