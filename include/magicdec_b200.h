@@ -139,12 +139,38 @@ MD_API size_t md_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_
  *   out: device fp32 [B][T][Hq][head_dim]; lse: device fp32 [B][T][Hq] or NULL.
  *   workspace: zero-initialised device scratch of >= md_attn_workspace_bytes(B, Hq, Hkv, d, T,
  *              max_kv_len) bytes.
- * Supported: head_dim in {64, 128}, g*T <= 64, 1 <= T <= 16.
+ * Supported: head_dim in {64, 128}, 1 <= T <= 16, g*T <= 128 query rows per KV head at head_dim 128
+ * (the tcgen05 kernel) and g*T <= 64 at head_dim 64.
  * Preconditions (device): T <= kv_len[b] <= min(max_kv_len, capacity).
  */
 MD_API md_status md_verify_attn_full(const md_kv_cache* cache, const void* q, int32_t num_q_heads, int32_t T,
                               const int32_t* kv_len, int32_t max_kv_len, float scale, float* out, float* lse,
                               void* workspace, size_t workspace_bytes, md_stream_t stream);
+
+/*
+ * md_verify_attn_full_det / md_draft_attn_sparse_det — the same results as md_verify_attn_full /
+ * md_draft_attn_sparse (same definition, tolerance and limits), computed with a DETERMINISTIC
+ * fixed-split plan: every (sequence, KV head) unit's key sequence is cut at multiples of
+ * `split_keys` (a multiple of 64), each piece is reduced by one CTA and the pieces' partials are
+ * merged in piece order (the log-sum-exp combination of SURVEY §8(a) row a4).  The bits of a unit's
+ * output then depend only on that unit's inputs and on split_keys -- not on the GPU's SM count,
+ * the other sequences or KV heads, or how a batch is sharded over ranks: a KV-head tensor-parallel
+ * or batch-sharded run reproduces the single-GPU output bit for bit (SURVEY §8(e) MD_FIXED_SPLIT).
+ * The stream-K plan of the plain calls balances bytes across SMs instead and is the faster one.
+ *   workspace: zero-initialised, >= md_attn_workspace_bytes_det(B, Hq, Hkv, d, T, max_keys,
+ *              split_keys) bytes, max_keys = max_kv_len (verify) or min(sink + window, capacity)
+ *              (draft; T = 1).  Returns 0 for invalid args.
+ */
+MD_API size_t md_attn_workspace_bytes_det(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads, int32_t head_dim,
+                                          int32_t T, int32_t max_keys, int32_t split_keys);
+MD_API md_status md_verify_attn_full_det(const md_kv_cache* cache, const void* q, int32_t num_q_heads, int32_t T,
+                                         const int32_t* kv_len, int32_t max_kv_len, int32_t split_keys, float scale,
+                                         float* out, float* lse, void* workspace, size_t workspace_bytes,
+                                         md_stream_t stream);
+MD_API md_status md_draft_attn_sparse_det(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                          const int32_t* kv_len, int32_t sink, int32_t window, int32_t split_keys,
+                                          float scale, float* out, float* lse, void* workspace,
+                                          size_t workspace_bytes, md_stream_t stream);
 
 /*
  * md_verify_attn_tree — verification of a token TREE of T nodes per sequence (f3; the

@@ -32,7 +32,8 @@ ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_works
                "md_pq_select", "md_verify_attn_full_tp", "md_draft_attn_sparse_tp", "md_tp_barrier",
                "md_philox_u32_dev", "md_draft_attn_sparse_windows", "md_verify_attn_full_append",
                "md_draft_attn_sparse_append", "md_verify_attn_full_tp_append", "md_draft_attn_sparse_tp_append",
-               "md_draft_attn_indexed_append")
+               "md_draft_attn_indexed_append", "md_attn_workspace_bytes_det", "md_verify_attn_full_det",
+               "md_draft_attn_sparse_det")
 
 
 class MDError(RuntimeError):
@@ -118,6 +119,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                                    ptp, c_void_p, c_void_p, sz, c_void_p]
     lib.md_tp_barrier.argtypes = [psync, c_void_p]
     lib.md_philox_u32_dev.argtypes = [u64, c_void_p, i32, i32, c_void_p, c_void_p]
+    lib.md_attn_workspace_bytes_det.argtypes = [i32, i32, i32, i32, i32, i32, i32]
+    lib.md_attn_workspace_bytes_det.restype = sz
+    lib.md_verify_attn_full_det.argtypes = [pc, c_void_p, i32, i32, c_void_p, i32, i32, f32, c_void_p, c_void_p,
+                                            c_void_p, sz, c_void_p]
+    lib.md_draft_attn_sparse_det.argtypes = [pc, c_void_p, i32, c_void_p, i32, i32, i32, f32, c_void_p, c_void_p,
+                                             c_void_p, sz, c_void_p]
     lib.md_pq_encode.argtypes = [pc, c_void_p, c_void_p, i32, c_void_p, i32, c_void_p]
     lib.md_pq_workspace_bytes.argtypes = [i32, i32, i32]
     lib.md_pq_workspace_bytes.restype = sz
@@ -191,6 +198,34 @@ def verify_attn_full(q, k_cache, v_cache, kv_len, max_kv_len, scale, out, lse=No
     ws, wsb = _ws(workspace)
     _check(lib.md_verify_attn_full(ctypes.byref(c), _ptr(q), q.shape[2], q.shape[1], _ptr(kv_len), int(max_kv_len),
                                    float(scale), _ptr(out), _ptr(lse), ws, wsb, _stream(stream)))
+
+
+def attn_workspace_bytes_det(batch, num_q_heads, num_kv_heads, head_dim, T, max_keys, split_keys) -> int:
+    return int(load_library().md_attn_workspace_bytes_det(batch, num_q_heads, num_kv_heads, head_dim, T, max_keys,
+                                                          split_keys))
+
+
+def verify_attn_full_det(q, k_cache, v_cache, kv_len, max_kv_len, split_keys, scale, out, lse=None, workspace=None,
+                         stream=None):
+    """verify_attn_full with the deterministic fixed-split plan (bits independent of the grid and
+    of sharding); workspace from attn_workspace_bytes_det."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_verify_attn_full_det(ctypes.byref(c), _ptr(q), q.shape[2], q.shape[1], _ptr(kv_len),
+                                       int(max_kv_len), int(split_keys), float(scale), _ptr(out), _ptr(lse), ws, wsb,
+                                       _stream(stream)))
+
+
+def draft_attn_sparse_det(q, k_cache, v_cache, kv_len, sink, window, split_keys, scale, out, lse=None,
+                          workspace=None, stream=None):
+    """draft_attn_sparse with the deterministic fixed-split plan."""
+    lib = load_library()
+    c = make_cache(k_cache, v_cache)
+    ws, wsb = _ws(workspace)
+    _check(lib.md_draft_attn_sparse_det(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(kv_len), int(sink), int(window),
+                                        int(split_keys), float(scale), _ptr(out), _ptr(lse), ws, wsb,
+                                        _stream(stream)))
 
 
 def verify_attn_tree(q, k_cache, v_cache, kv_len, max_kv_len, tree_mask, scale, out, lse=None, workspace=None,

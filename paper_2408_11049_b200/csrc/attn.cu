@@ -95,6 +95,12 @@ struct AttnParams {
   int64_t c_sB, c_sH, c_sS;        // cache strides in elements
   int mode;
   float scale_log2;       // scale * log2(e)
+  // deterministic fixed-split plan (md_*_det): every unit is cut at multiples of det_split tiles,
+  // each piece is one segment with its own partial slot (unit * det_maxp + piece), merged in
+  // piece order -> results independent of the grid, of the other units and of how the batch or
+  // the KV heads are sharded.  0: the stream-K plan.
+  int det_split;
+  int det_maxp;
 };
 
 // ------------------------------------------------------------------ stream-K decomposition
@@ -252,6 +258,7 @@ struct SegWalker {
     sg.ustart = ustart;
     sg.lo = static_cast<int>(t - ustart);
     sg.hi = static_cast<int>(min(end, ustart + tiles_b) - ustart);
+    if (p.det_split > 0) sg.hi = min(sg.hi, (sg.lo / p.det_split + 1) * p.det_split);  // one piece per segment
     t = ustart + sg.hi;
     if (sg.hi == tiles_b) {  // advance to the next unit (skipping empty sequences)
       ustart += tiles_b;
@@ -266,6 +273,33 @@ struct SegWalker {
     return true;
   }
 };
+
+// Deterministic plan: a nominal CTA boundary t of the tile space moves forward to the next piece
+// boundary of the unit that holds it (ustart + k * det_split, or the unit's end), so every piece
+// is processed whole by one CTA.  A pure function of t: neighbouring CTAs agree on it.
+__device__ int64_t det_snap(const AttnParams& p, const int* pre, int64_t t, int64_t total) {
+  if (p.det_split <= 0 || t >= total) return t;
+  SegWalker w;
+  w.init(p, pre, t, total);
+  if (w.t >= w.end) return total;
+  const int64_t rel = t - w.ustart;
+  const int64_t snapped = w.ustart + (rel + p.det_split - 1) / p.det_split * p.det_split;
+  return min(snapped, w.ustart + (int64_t)w.tiles_b);
+}
+// this CTA's static range [S, E) of the tile space (chunk = blockIdx.x)
+__device__ __forceinline__ void cta_range(const AttnParams& p, const int* pre, const Plan& pl, int chunk, int64_t& S,
+                                          int64_t& E) {
+  S = pl.start(chunk);
+  E = pl.start(chunk + 1);
+  if (p.det_split > 0) {
+    S = det_snap(p, pre, S, pl.total);
+    E = det_snap(p, pre, E, pl.total);
+  }
+}
+// partial slot of a segment that does not complete its unit
+__device__ __forceinline__ int seg_slot(const AttnParams& p, const Plan& pl, const Seg& sg, int chunk) {
+  return p.det_split > 0 ? sg.unit * p.det_maxp + sg.lo / p.det_split : chunk * 2 + pl.slot(sg.ustart, chunk);
+}
 
 // Key ranges [s0, e0) then [s1, e1) of the segment's logical keys.  Part 1 is always a range
 // of cache rows; part 0 is a range of cache rows too, except in MODE_INDEXED where it is a
@@ -480,7 +514,16 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
 template <int D>
 __device__ void finish_unit(const AttnParams& p, const Seg& sg, const Plan& pl, int nthr, int* flag) {
   named_bar_sync(1, nthr);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && p.det_split > 0) {  // deterministic plan: pieces 0 .. np-1 of the unit
+    const int np = (sg.tiles + p.det_split - 1) / p.det_split;
+    const int old = atomic_add_acq_rel_gpu(p.counters + sg.unit, 1);
+    const int last = (old == np - 1);
+    if (last) p.counters[sg.unit] = 0;
+    flag[0] = last;
+    flag[1] = 0;
+    flag[2] = np - 1;
+    flag[3] = 0;
+  } else if (threadIdx.x == 0) {
     const int cf = pl.chunk_of(sg.ustart), cl = pl.chunk_of(sg.ustart + sg.tiles - 1);
     const int old = atomic_add_acq_rel_gpu(p.counters + sg.unit, 1);
     const int last = (old == cl - cf);
@@ -504,7 +547,8 @@ __device__ void finish_unit(const AttnParams& p, const Seg& sg, const Plan& pl, 
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 2
     for (int c = cf; c <= cl; ++c) {
-      const int64_t prow = ((int64_t)c * 2 + (c == cf ? s0 : 0)) * p.R + r;
+      const int64_t prow = (p.det_split > 0 ? (int64_t)sg.unit * p.det_maxp + c : (int64_t)c * 2 + (c == cf ? s0 : 0)) *
+                               p.R + r;
       const float ls = __ldcg(p.ws_lse + prow);
       const float4 v = __ldcg(reinterpret_cast<const float4*>(p.ws_o + prow * D + c4));
       if (ls == -INFINITY) continue;  // an empty partial
@@ -594,7 +638,11 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
   if ((int)blockIdx.x >= pl.G) return;  // uniform across the CTA
   int chunk = blockIdx.x;                // this CTA's static chunk, then claimed dynamic ones
   SegWalker walk;
-  walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+  {
+    int64_t S0, E0;
+    cta_range(p, pre, pl, chunk, S0, E0);
+    walk.init(p, pre, S0, E0);
+  }
   Seg sg;
   trace_stamp(p, 2);
 
@@ -866,7 +914,7 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
     }
     // rows r < R -> the final output, or this chunk's partial slot
     const bool complete = sg.complete();
-    const int slot_base = chunk * 2 + pl.slot(sg.ustart, chunk);
+    const int slot_base = seg_slot(p, pl, sg, chunk);
     if (ks == 0) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -995,7 +1043,11 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   if ((int)blockIdx.x >= pl.G) return;  // uniform across the CTA
   int chunk = blockIdx.x;                // this CTA's static chunk, then claimed dynamic ones
   SegWalker walk;
-  walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+  {
+    int64_t S0, E0;
+    cta_range(p, pre, pl, chunk, S0, E0);
+    walk.init(p, pre, S0, E0);
+  }
   Seg sg;
   trace_stamp(p, 2);
   if (p.kn != nullptr && warp < NC) {  // fused append: the new rows of this CTA's tiles
@@ -1283,7 +1335,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     trace_stamp(p, 7);
     // rows r < R -> the final output, or this CTA's partial slot
     const bool complete = sg.complete();
-    const int slot_base = chunk * 2 + pl.slot(sg.ustart, chunk);
+    const int slot_base = seg_slot(p, pl, sg, chunk);
     {
       constexpr int V4 = D / 4;
       for (int idx = threadIdx.x; idx < p.R * V4; idx += NC * 32) {
@@ -1357,13 +1409,18 @@ static int dyn_k_for(int R) { return use_keys_kernel(R) ? DYN_K : 0; }
 // one workspace: no call's partials ever overlap another call's counters.
 constexpr int MAX_UNITS = 65536;  // B * Hkv
 constexpr size_t COUNTER_BYTES = ((size_t)(MAX_UNITS + 2) * 4 + 255) & ~size_t(255);
-static size_t workspace_for(int G, int units, int R, int D) {
-  (void)units;
-  // partial slots for the mma.sync kernels' grid, or the tcgen05 kernel's (1 CTA / SM, dynamic
-  // chunks), whichever is larger (the workspace query does not know which kernel will run)
-  const size_t C = std::max((size_t)G * (1 + dyn_k_for(R)), (size_t)device_sm_count());
+// partial slots: two per work chunk of the stream-K plan (the mma.sync kernels' grid with its
+// dynamic chunks, or the tcgen05 kernel's 1 CTA / SM, whichever is larger: the workspace query
+// does not know which kernel will run), or, for the deterministic plan, one per piece
+// (units * det_maxp)
+static size_t partial_slots(int G, int units, int R, int det_maxp) {
+  if (det_maxp > 0) return (size_t)units * det_maxp;
+  return 2 * std::max((size_t)G * (1 + dyn_k_for(R)), (size_t)device_sm_count());
+}
+static size_t workspace_for(int G, int units, int R, int D, int det_maxp = 0) {
+  const size_t C = partial_slots(G, units, R, det_maxp);
   const size_t X = use_keys_kernel(R) ? 0 : (size_t)G * XS_FRAGS * 16 * D * 4;  // rows-kernel scratch
-  return COUNTER_BYTES + align256(C * 2 * R * D * 4) + align256(C * 2 * R * 4) + align256(X);
+  return COUNTER_BYTES + align256(C * R * D * 4) + align256(C * R * 4) + align256(X);
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -1494,7 +1551,8 @@ struct IndexedArgs {
   const int32_t* windows = nullptr;     // draft: per-sequence windows
   const void* k_new = nullptr;          // fused append (md_*_append): [B][T][Hkv][d] rows for [n-T, n)
   const void* v_new = nullptr;
-  int max_keys = 0;                     // fused append: upper bound of the keys per unit (plan choice)
+  int max_keys = 0;                     // fused append / det: upper bound of the keys per unit (plan choice)
+  int det_split_tiles = 0;              // deterministic fixed-split plan (md_*_det): piece length in tiles
 };
 
 static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int T, const int32_t* kv_len, int sink,
@@ -1525,7 +1583,10 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
              units, MAX_UNITS);
   const bool tcg = use_tc_kernel(R, c->head_dim, mode);
   const int grid = grid_for(R, device_sm_count(), tcg);
-  const size_t need = workspace_for(grid, units, R, c->head_dim);
+  const int det_maxp = ix.det_split_tiles > 0
+                           ? (int)(((int64_t)(ix.max_keys + TK - 1) / TK + ix.det_split_tiles - 1) / ix.det_split_tiles)
+                           : 0;
+  const size_t need = workspace_for(grid, units, R, c->head_dim, det_maxp);
   MD_REQUIRE(ws != nullptr && ws_bytes >= need, MD_ERR_WORKSPACE, "%s: workspace of %zu bytes required, %zu given",
              who, need, ws_bytes);
   TmapSet tm;
@@ -1598,15 +1659,18 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   if (fuse_append) p.dyn_k = 0;  // the new rows are written per static range (append_own_rows)
   p.dyn_static_permille = DYN_STATIC_PERMILLE;
   p.dyn_min_tiles = DYN_MIN_TILES;
-  const size_t chunks = (size_t)grid * (1 + p.dyn_k);
+  p.det_split = ix.det_split_tiles;
+  p.det_maxp = det_maxp;
+  if (p.det_split > 0) p.dyn_k = 0;
+  const size_t slots = partial_slots(grid, units, R, det_maxp);
   uint8_t* w = static_cast<uint8_t*>(ws);
   p.dyn = reinterpret_cast<int*>(w);
   p.counters = p.dyn + 2;
   w += COUNTER_BYTES;
   p.ws_o = reinterpret_cast<float*>(w);
-  w += align256(chunks * 2 * R * c->head_dim * 4);
+  w += align256(slots * R * c->head_dim * 4);
   p.ws_lse = reinterpret_cast<float*>(w);
-  w += align256(chunks * 2 * R * 4);
+  w += align256(slots * R * 4);
   p.ws_x = use_keys_kernel(R) ? nullptr : reinterpret_cast<float*>(w);
   p.pdl_early = 1;  // keys kernel: trigger the dependent launch at entry
   if (tcg) {
@@ -1859,6 +1923,55 @@ extern "C" md_status md_draft_attn_indexed_append(const md_kv_cache* cache, cons
   ix.v_new = v_new;
   return run_attention(cache, q, num_q_heads, 1, kv_len, 0, 0, MODE_INDEXED, scale, out, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_draft_attn_indexed_append", ix);
+}
+
+extern "C" size_t md_attn_workspace_bytes_det(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
+                                              int32_t head_dim, int32_t T, int32_t max_keys, int32_t split_keys) {
+  using namespace md;
+  if (batch < 1 || num_kv_heads < 1 || num_q_heads < 1 || num_q_heads % num_kv_heads || T < 1 || max_keys < 1 ||
+      (head_dim != 64 && head_dim != 128) || split_keys < TK || split_keys % TK)
+    return 0;
+  const int R = (num_q_heads / num_kv_heads) * T;
+  const int S = split_keys / TK;
+  const int maxp = (int)(((int64_t)(max_keys + TK - 1) / TK + S - 1) / S);
+  return workspace_for(grid_for(R, device_sm_count()), batch * num_kv_heads, R, head_dim, maxp);
+}
+
+extern "C" md_status md_verify_attn_full_det(const md_kv_cache* cache, const void* q, int32_t num_q_heads, int32_t T,
+                                             const int32_t* kv_len, int32_t max_kv_len, int32_t split_keys,
+                                             float scale, float* out, float* lse, void* workspace,
+                                             size_t workspace_bytes, md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(T >= 1 && T <= 16, MD_ERR_UNSUPPORTED, "md_verify_attn_full_det: T must be in [1, 16]");
+  MD_REQUIRE(cache != nullptr, MD_ERR_INVALID_ARG, "md_verify_attn_full_det: NULL cache");
+  MD_REQUIRE(max_kv_len >= T && max_kv_len <= cache->capacity, MD_ERR_INVALID_ARG,
+             "md_verify_attn_full_det: need T <= max_kv_len <= capacity");
+  MD_REQUIRE(split_keys >= TK && split_keys % TK == 0, MD_ERR_INVALID_ARG,
+             "md_verify_attn_full_det: split_keys must be a positive multiple of 64");
+  IndexedArgs ix;
+  ix.det_split_tiles = split_keys / TK;
+  ix.max_keys = max_kv_len;
+  return run_attention(cache, q, num_q_heads, T, kv_len, 0, 0, MODE_VERIFY, scale, out, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_verify_attn_full_det", ix);
+}
+
+extern "C" md_status md_draft_attn_sparse_det(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                              const int32_t* kv_len, int32_t sink, int32_t window,
+                                              int32_t split_keys, float scale, float* out, float* lse,
+                                              void* workspace, size_t workspace_bytes, md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(cache != nullptr, MD_ERR_INVALID_ARG, "md_draft_attn_sparse_det: NULL cache");
+  MD_REQUIRE(sink >= 0 && window >= 0 && (int64_t)sink + window >= 1, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_det: need sink >= 0, window >= 0, sink + window >= 1");
+  MD_REQUIRE(split_keys >= TK && split_keys % TK == 0, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_det: split_keys must be a positive multiple of 64");
+  IndexedArgs ix;
+  ix.det_split_tiles = split_keys / TK;
+  ix.max_keys = (int)std::min<int64_t>((int64_t)sink + window, cache->capacity);
+  return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, out, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_det", ix);
 }
 
 extern "C" MD_API md_status md_debug_trace(void* buf, size_t bytes) {

@@ -275,7 +275,11 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
   const bool active = (int)blockIdx.x < pl.G;
   SegWalker walk;
   Seg sg;
-  if (active) walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+  if (active) {
+    int64_t S0, E0;
+    cta_range(p, pre, pl, chunk, S0, E0);
+    walk.init(p, pre, S0, E0);
+  }
   if (p.kn != nullptr && warp < 4 && active) {  // fused append: the new rows of this CTA's tiles
     append_own_rows<128>(p, pre, pl.start(chunk), pl.start(chunk + 1), threadIdx.x, 128);
     __syncwarp();
@@ -523,7 +527,7 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
       if (lane == 0) mbar_arrive(&oempty[ob]);
       bar128();
       const bool complete = sg.complete();
-      const int slot_base = chunk * 2 + pl.slot(sg.ustart, chunk);
+      const int slot_base = seg_slot(p, pl, sg, chunk);
 #pragma unroll
       for (int r = 0; r < NP; ++r) {
         if (r < R) {
@@ -720,7 +724,7 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
       mbar_wait(&ofull[ob], (si >> 1) & 1);
       fence_after();
       const bool complete = sg.complete();
-      const int slot_base = chunk * 2 + pl.slot(sg.ustart, chunk);
+      const int slot_base = seg_slot(p, pl, sg, chunk);
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
         float o[CH];
