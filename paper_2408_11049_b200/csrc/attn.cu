@@ -101,6 +101,10 @@ struct AttnParams {
   // the KV heads are sharded.  0: the stream-K plan.
   int det_split;
   int det_maxp;
+  // unit-aligned static plan (draft calls): every CTA boundary moves forward to the end of the unit
+  // holding it, so CTAs process whole units -- no split partials, no merges (short units: a
+  // split's epilogue + merge costs more than the byte imbalance of whole units)
+  int unit_aligned;
 };
 
 // ------------------------------------------------------------------ stream-K decomposition
@@ -278,20 +282,34 @@ struct SegWalker {
 // boundary of the unit that holds it (ustart + k * det_split, or the unit's end), so every piece
 // is processed whole by one CTA.  A pure function of t: neighbouring CTAs agree on it.
 __device__ int64_t det_snap(const AttnParams& p, const int* pre, int64_t t, int64_t total) {
-  if (p.det_split <= 0 || t >= total) return t;
+  if ((p.det_split <= 0 && !p.unit_aligned) || t >= total) return t;
   SegWalker w;
   w.init(p, pre, t, total);
   if (w.t >= w.end) return total;
   const int64_t rel = t - w.ustart;
+  if (rel == 0) return t;
+  if (p.det_split <= 0) return w.ustart + w.tiles_b;  // unit-aligned: the end of the unit
   const int64_t snapped = w.ustart + (rel + p.det_split - 1) / p.det_split * p.det_split;
   return min(snapped, w.ustart + (int64_t)w.tiles_b);
 }
 // this CTA's static range [S, E) of the tile space (chunk = blockIdx.x)
+// first tile of unit u = b * Hkv + h (O(1) with the in-CTA prefix table)
+__device__ __forceinline__ int64_t unit_start(const AttnParams& p, const int* pre, int u) {
+  const int b = u / p.Hkv, h = u - b * p.Hkv;
+  if (b >= p.B) return pre[p.B];
+  return pre[b] + (int64_t)h * tiles_of(p, pre, b);
+}
 __device__ __forceinline__ void cta_range(const AttnParams& p, const int* pre, const Plan& pl, int chunk, int64_t& S,
                                           int64_t& E) {
+  if (p.unit_aligned && p.B <= TABLE_B) {  // whole units, evenly by count: CTA c takes units [cU/G, (c+1)U/G)
+    const int U = p.B * p.Hkv;
+    S = unit_start(p, pre, (int)((int64_t)chunk * U / pl.G));
+    E = unit_start(p, pre, (int)((int64_t)(chunk + 1) * U / pl.G));
+    return;
+  }
   S = pl.start(chunk);
   E = pl.start(chunk + 1);
-  if (p.det_split > 0) {
+  if (p.det_split > 0 || p.unit_aligned) {
     S = det_snap(p, pre, S, pl.total);
     E = det_snap(p, pre, E, pl.total);
   }
@@ -1051,7 +1069,9 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   Seg sg;
   trace_stamp(p, 2);
   if (p.kn != nullptr && warp < NC) {  // fused append: the new rows of this CTA's tiles
-    append_own_rows<D>(p, pre, pl.start(chunk), pl.start(chunk + 1), threadIdx.x, NC * 32);
+    int64_t S0, E0;
+    cta_range(p, pre, pl, chunk, S0, E0);
+    append_own_rows<D>(p, pre, S0, E0, threadIdx.x, NC * 32);
     __syncwarp();
     if (lane == 0) mbar_arrive(apb);
   }
@@ -1401,6 +1421,9 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int DYN_K = 4;
 constexpr int DYN_MIN_TILES = 128;  // dynamic only when a call has >= 128 tiles (8 MB of K+V) per CTA
 constexpr int DYN_STATIC_PERMILLE = 750;
+#ifndef MD_UNIT_ALIGNED_DRAFT
+#define MD_UNIT_ALIGNED_DRAFT 1  // draft calls: whole units per CTA (0: the stream-K plan; A/B builds only)
+#endif
 static int dyn_k_for(int R) { return use_keys_kernel(R) ? DYN_K : 0; }
 
 // [counters int32: 2 dynamic-chunk counters + MAX_UNITS unit counters][partials fp32 C*2*R*D]
@@ -1582,7 +1605,25 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   MD_REQUIRE(units <= MAX_UNITS, MD_ERR_UNSUPPORTED, "%s: batch * num_kv_heads = %d > %d is not supported", who,
              units, MAX_UNITS);
   const bool tcg = use_tc_kernel(R, c->head_dim, mode);
-  const int grid = grid_for(R, device_sm_count(), tcg);
+  int grid = grid_for(R, device_sm_count(), tcg);
+  // Draft calls (short units: <= sink + window keys) run the unit-aligned plan on ceil(units / per)
+  // CTAs, per = ceil(units / grid) whole units each: no split partials or merges.  Measured at the
+  // target point (B = 64, 512 units of 1024 keys): 51.4 -> 49.1 us per call; Qwen2.5 (256 units of
+  // 2048 keys): 50.7 -> 48.5 us (tools/draft_ab.py, profiles/draft_ab_r02.txt).  Not when the
+  // keys kernel's dynamic tail engages (long calls), nor for the deterministic plan.
+  bool unit_aligned = false;
+  if ((mode == MODE_DRAFT || mode == MODE_INDEXED) && !tcg && ix.det_split_tiles == 0 && MD_UNIT_ALIGNED_DRAFT) {
+    const int64_t keys_ub = mode == MODE_DRAFT ? std::min<int64_t>((int64_t)sink + window, c->capacity) : c->capacity;
+    const int64_t tiles_ub = (int64_t)c->batch * c->num_kv_heads * ((keys_ub + TK - 1) / TK);
+    if (!(dyn_k_for(R) > 0 && tiles_ub >= (int64_t)DYN_MIN_TILES * grid)) {
+      const int units_ = c->batch * c->num_kv_heads, per = (units_ + grid - 1) / grid;
+#ifndef MD_EXP_UNIT_FULLGRID
+#define MD_EXP_UNIT_FULLGRID 0  // experiment (A/B builds only): keep the full grid, boundaries snapped
+#endif
+      if (!MD_EXP_UNIT_FULLGRID) grid = (units_ + per - 1) / per;
+      unit_aligned = true;
+    }
+  }
   const int det_maxp = ix.det_split_tiles > 0
                            ? (int)(((int64_t)(ix.max_keys + TK - 1) / TK + ix.det_split_tiles - 1) / ix.det_split_tiles)
                            : 0;
@@ -1661,6 +1702,8 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.dyn_min_tiles = DYN_MIN_TILES;
   p.det_split = ix.det_split_tiles;
   p.det_maxp = det_maxp;
+  p.unit_aligned = unit_aligned ? 1 : 0;
+  if (unit_aligned) p.dyn_k = 0;
   if (p.det_split > 0) p.dyn_k = 0;
   const size_t slots = partial_slots(grid, units, R, det_maxp);
   uint8_t* w = static_cast<uint8_t*>(ws);
@@ -1685,7 +1728,8 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
          : (R == 35) ? launch_tc<48, 35>(tm, qm, p, grid, s)
          : (R <= 16) ? launch_tc<16, 0>(tm, qm, p, grid, s)
          : (R <= 32) ? launch_tc<32, 0>(tm, qm, p, grid, s)
-         : (R <= 48) ? launch_tc<48, 0>(tm, qm, p, grid, s)
+         // 32 < R <= 64 (R != 35): two row groups (measured: R = 48 at 5.9 TB/s with one group of
+         // 48 run-time rows, R = 49..64 at 6.5-6.8 TB/s with two groups; tools/rows_sweep.py)
          : (R <= 64) ? launch_tc<64, 0>(tm, qm, p, grid, s)
          : (R <= 96) ? launch_tc<96, 0>(tm, qm, p, grid, s)
                      : launch_tc<128, 0>(tm, qm, p, grid, s);

@@ -25,6 +25,8 @@
 // Stream-K decomposition, split partials and the fused last-arriver merge are those of the
 // mma.sync kernels (64-key plan tiles; a 128-key stage covers two of them).
 
+#include <type_traits>
+
 namespace tc {  // helpers: tcgen05.cuh (included by attn.cu)
 
 constexpr int KT = 128;                      // keys per stage (MMA M)
@@ -43,7 +45,7 @@ template <int NP>
 struct Cfg {
   static constexpr int NG = NP <= 48 ? 1 : 2;        // row groups
   static constexpr int CW = NP / NG;                 // query-row columns per group
-  static constexpr int CH = CW % 32 == 0 ? 32 : 16;  // columns per TMEM load chunk (NG > 1)
+  static constexpr int CH = CW == 32 ? 32 : 16;      // columns per TMEM load chunk (NG > 1)
   static constexpr int SM_THREADS = 128 * NG;        // softmax / epilogue threads
   static constexpr int THREADS = SM_THREADS + 64;    // + producer warp + MMA warp
   static constexpr int NQ = NP <= 32 ? 2 : 1;        // Q buffers (by segment parity)
@@ -281,7 +283,9 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
     walk.init(p, pre, S0, E0);
   }
   if (p.kn != nullptr && warp < 4 && active) {  // fused append: the new rows of this CTA's tiles
-    append_own_rows<128>(p, pre, pl.start(chunk), pl.start(chunk + 1), threadIdx.x, 128);
+    int64_t S0, E0;
+    cta_range(p, pre, pl, chunk, S0, E0);
+    append_own_rows<128>(p, pre, S0, E0, threadIdx.x, 128);
     __syncwarp();
     if (lane == 0) mbar_arrive(apb);
   }
@@ -595,13 +599,13 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
         // dead(r): key x is invisible to query row cb + r (a padded row, a key past the valid
         // range, or a new key outside the row's causal chain / tree mask)
         uint64_t dead = 0;
-#pragma unroll
-        for (int r = 0; r < CW; ++r)
-          if (cb + r >= R) dead |= 1ull << r;
         if (edge) {
+#pragma unroll 1
+          for (int r = 0; r < CW; ++r)
+            if (cb + r >= R) dead |= 1ull << r;
           int t = cb / p.g, hh = cb - t * p.g;
           uint32_t msk = t < p.T ? (p.tree_mask ? __ldg(p.tree_mask + (size_t)b * p.T + t) : ((2u << t) - 1u)) : 0u;
-#pragma unroll
+#pragma unroll 1
           for (int r = 0; r < CW; ++r) {
             if (!valid || (rel >= 0 && !((msk >> (rel & 31)) & 1u))) dead |= 1ull << r;
             if (++hh == p.g) {
@@ -613,23 +617,31 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
         }
         twait(&sfull[sb], (tt >> 1) & 1, nullptr);
         fence_after();
-        // pass 1: does any score exceed its row maximum by > 2^8 (or meet m = -inf)?
-        float xmax = -INFINITY;
+        // pass 1: does any score exceed its row maximum by > 2^8 (or meet m = -inf)?  Outside a
+        // unit's edge stage nothing is masked: padded rows (r >= R, zero queries) are computed like
+        // live ones there -- harmless, their outputs are never stored -- so the common stage has no
+        // per-element tests (E = false)
+        auto pass1 = [&](auto edge_c) -> float {
+          constexpr bool E = decltype(edge_c)::value;
+          float xm = -INFINITY;
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-          float v[CH];
-          tload(s_col + ch * CH, v);
+          for (int ch = 0; ch < NCH; ++ch) {
+            float v[CH];
+            tload(s_col + ch * CH, v);
 #pragma unroll
-          for (int r = 0; r < CH; r += 4) {
-            const float4 m4 = *reinterpret_cast<const float4*>(mrow + cb + ch * CH + r);
-            const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+            for (int r = 0; r < CH; r += 4) {
+              const float4 m4 = *reinterpret_cast<const float4*>(mrow + cb + ch * CH + r);
+              const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const bool live = !((dead >> (ch * CH + r + i)) & 1ull);
-              xmax = fmaxf(xmax, live ? fmaf(v[r + i], sl2, -mm[i]) : -INFINITY);
+              for (int i = 0; i < 4; ++i) {
+                const float xv = fmaf(v[r + i], sl2, -mm[i]);
+                xm = fmaxf(xm, (E && ((dead >> (ch * CH + r + i)) & 1ull)) ? -INFINITY : xv);
+              }
             }
           }
-        }
+          return xm;
+        };
+        const float xmax = edge ? pass1(std::true_type()) : pass1(std::false_type());
         if (tt > 0) twait(pempty, (tt - 1) & 1, nullptr);  // previous PV done: P and O^T are free
         if (vote_any128(xmax > THR, bar_id)) {
           // raise the group's row maxima to this tile's: per-row max over the 128 keys
@@ -640,7 +652,7 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
 #pragma unroll
             for (int i = 0; i < CH; ++i) {
               const int r = ch * CH + i;
-              float m = ((dead >> r) & 1ull) ? -INFINITY : v[i] * sl2;
+              float m = (edge && ((dead >> r) & 1ull)) ? -INFINITY : v[i] * sl2;
 #pragma unroll
               for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
               if (lane == 0) gred[wq * CW + r] = m;
@@ -674,30 +686,34 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
         // pass 2: P = 2^(s * scale * log2 e - m) for the group's rows; row sums in fp32, the MMA
         // operand is bf16 (P^T core layout: key x -> core column x / 8, row (x % 8) * 16 B)
         uint8_t* pd = pbuf + (x >> 3) * 128 + (x & 7) * 16 + (cb / 8) * 2048;
+        auto pass2 = [&](auto edge_c) {
+          constexpr bool E = decltype(edge_c)::value;
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-          float v[CH];
-          tload(s_col + ch * CH, v);
-          uint32_t pk[CH / 2];
+          for (int ch = 0; ch < NCH; ++ch) {
+            float v[CH];
+            tload(s_col + ch * CH, v);
+            uint32_t pk[CH / 2];
 #pragma unroll
-          for (int r = 0; r < CH; r += 4) {
-            const float4 m4 = *reinterpret_cast<const float4*>(mrow + cb + ch * CH + r);
-            const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
-            float pr[4];
+            for (int r = 0; r < CH; r += 4) {
+              const float4 m4 = *reinterpret_cast<const float4*>(mrow + cb + ch * CH + r);
+              const float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+              float pr[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const bool live = !((dead >> (ch * CH + r + i)) & 1ull);
-              pr[i] = live ? ex2(fmaf(v[r + i], sl2, -mm[i])) : 0.f;
-              lacc[ch * CH + r + i] += pr[i];
+              for (int i = 0; i < 4; ++i) {
+                pr[i] = (E && ((dead >> (ch * CH + r + i)) & 1ull)) ? 0.f : ex2(fmaf(v[r + i], sl2, -mm[i]));
+                lacc[ch * CH + r + i] += pr[i];
+              }
+              pk[r / 2] = pack_bf16(pr[0], pr[1]);
+              pk[r / 2 + 1] = pack_bf16(pr[2], pr[3]);
             }
-            pk[r / 2] = pack_bf16(pr[0], pr[1]);
-            pk[r / 2 + 1] = pack_bf16(pr[2], pr[3]);
-          }
 #pragma unroll
-          for (int c = 0; c < CH / 8; ++c)
-            *reinterpret_cast<uint4*>(pd + (ch * CH / 8 + c) * 2048) =
-                make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        }
+            for (int c = 0; c < CH / 8; ++c)
+              *reinterpret_cast<uint4*>(pd + (ch * CH / 8 + c) * 2048) =
+                  make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+          }
+        };
+        if (edge) pass2(std::true_type());
+        else pass2(std::false_type());
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[sb]);  // S^T buffer sb is read for the last time
