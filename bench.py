@@ -191,7 +191,10 @@ def init_dist(world, local_dev):
     import torch.distributed as dist
     if world == 1:
         return None
-    backend = os.environ.get("MD_DIST_BACKEND", "nccl" if torch.cuda.is_available() else "gloo")
+    # NCCL needs one GPU per rank: more ranks than GPUs (a world-2 run wrapped onto one GPU via
+    # LOCAL_RANK) take gloo with CPU-staged exchanges
+    wrapped = torch.cuda.is_available() and world > torch.cuda.device_count()
+    backend = os.environ.get("MD_DIST_BACKEND", "nccl" if torch.cuda.is_available() and not wrapped else "gloo")
     os.environ.setdefault("NCCL_DEBUG", "INFO")
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if backend == "nccl":
@@ -361,7 +364,8 @@ def run_gpu(args):
             torch.cuda.synchronize()
             ok = int(torch.equal(buf, ref))
         except Exception as e:  # noqa: BLE001 - any failure selects the NCCL path
-            print(f"rank {rank}: fused exchange unavailable ({type(e).__name__}: {e}); using NCCL", file=sys.stderr)
+            print(f"rank {rank}: fused exchange unavailable ({type(e).__name__}: {e}); using the {backend} all-gather",
+                  file=sys.stderr, flush=True)
             ok = 0
         if all_reduce_host([ok], "min")[0] == 1:
             exchange = "p2p"
@@ -602,8 +606,10 @@ def run_gpu(args):
             "roofline": {"bound": "hbm", "achieved": round(v_gbs, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(v_gbs / peak, 4), "traffic": traffic,
                          "kernel": ("md_verify_attn_full_append" if fused else "md_verify_attn_full")
-                         + " (attn_tc_kernel: tcgen05 MMAs with TMEM accumulators, stream-K persistent, fused split merge"
-                         + (", fused kv_append)" if fused else ")"),
+                         + ((" (attn_tc_kernel: tcgen05 MMAs with TMEM accumulators, stream-K persistent, fused split merge"
+                             if d == 128 and (Hq // Hkv) * T > 8 else
+                             " (attn_keys_kernel: mma.sync swap-AB, stream-K persistent with dynamic tail, fused split merge")
+                            + (", fused kv_append)" if fused else ")")),
                          "algorithmic_bytes_per_launch": vb, "ms_per_launch": round(v_ms, 4),
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}; a copy: read + write)"},
             "verify_gbs": round(v_gbs, 1),

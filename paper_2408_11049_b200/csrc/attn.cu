@@ -105,6 +105,10 @@ struct AttnParams {
   // holding it, so CTAs process whole units -- no split partials, no merges (short units: a
   // split's epilogue + merge costs more than the byte imbalance of whole units)
   int unit_aligned;
+  // dynamic whole-unit plan (draft calls): CTA c starts on unit c, the units >= G are claimed one
+  // at a time from an atomic counter (fast SMs take more units; nothing is split or merged); the
+  // fused append is then done by the producer warp right before it issues a tile holding a new row
+  int unit_dyn;
 };
 
 // ------------------------------------------------------------------ stream-K decomposition
@@ -198,6 +202,12 @@ __device__ Plan make_plan(const AttnParams& p, int64_t total, int grid) {
   pl.S0 = total;
   pl.CH = 1;
   pl.nch = pl.G;
+  if (p.unit_dyn) {  // chunks are units (cta_range): G = min(grid, units), units >= G are claimed
+    const int U = p.B * p.Hkv;
+    pl.G = min(grid, U);
+    pl.nch = U;
+    return pl;
+  }
   // short calls (few tiles per CTA, e.g. every draft call) stay static: extra segments and
   // hand-offs cost more there than the bandwidth imbalance they remove
   if (p.dyn_k > 0 && total >= (int64_t)p.dyn_min_tiles * pl.G) {
@@ -301,6 +311,11 @@ __device__ __forceinline__ int64_t unit_start(const AttnParams& p, const int* pr
 }
 __device__ __forceinline__ void cta_range(const AttnParams& p, const int* pre, const Plan& pl, int chunk, int64_t& S,
                                           int64_t& E) {
+  if (p.unit_dyn) {  // chunk c = unit c (static: c < G, claimed: c >= G)
+    S = unit_start(p, pre, chunk);
+    E = unit_start(p, pre, chunk + 1);
+    return;
+  }
   if (p.unit_aligned && p.B <= TABLE_B) {  // whole units, evenly by count: CTA c takes units [cU/G, (c+1)U/G)
     const int U = p.B * p.Hkv;
     S = unit_start(p, pre, (int)((int64_t)chunk * U / pl.G));
@@ -500,6 +515,22 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
         if (lane == 0) mbar_arrive(&full[stage]);
         continue;
       }
+      if (p.unit_dyn && p.kn != nullptr && tile_has_new(p, n, pos, nvalid)) {
+        // dynamic-unit plan: the producer warp writes the new rows of this tile itself (generic
+        // stores ordered before its own TMA reads by fence.proxy.async + __syncwarp)
+        constexpr int NV = D / 8;
+        const int a = max(pos, n - p.T), e = min(pos + nvalid, n);
+        const int64_t ubase = (int64_t)b * p.c_sB + (int64_t)kvh * p.c_sH;
+        for (int i = lane; i < (e - a) * NV; i += 32) {
+          const int r = a + i / NV, c = (i % NV) * 8;
+          const int64_t src = (((int64_t)b * p.T + (r - (n - p.T))) * p.Hkv + kvh) * D + c;
+          const int64_t dst = ubase + (int64_t)r * p.c_sS + c;
+          *reinterpret_cast<uint4*>(p.kw + dst) = __ldg(reinterpret_cast<const uint4*>(p.kn + src));
+          *reinterpret_cast<uint4*>(p.vw + dst) = __ldg(reinterpret_cast<const uint4*>(p.vn + src));
+        }
+        fence_proxy_async_global();
+        __syncwarp();
+      }
       if (lane != 0) continue;
       if (apb != nullptr && tile_has_new(p, n, pos, nvalid)) mbar_wait(apb, 0);  // fused append done
       mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
@@ -693,7 +724,11 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
         ++ck;
         if (nxt < 0) return false;
         chunk = nxt;
-        walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+        {
+          int64_t S_, E_;
+          cta_range(p, pre, pl, chunk, S_, E_);
+          walk.init(p, pre, S_, E_);
+        }
       }
       return true;
     };
@@ -718,7 +753,11 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
       ++ck;
       if (nxt < 0) return false;
       chunk = nxt;
-      walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+      {
+        int64_t S_, E_;
+        cta_range(p, pre, pl, chunk, S_, E_);
+        walk.init(p, pre, S_, E_);
+      }
     }
     return true;
   };
@@ -973,6 +1012,9 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
 // P^T operand is the bf16-packed S^T fragment transposed in registers (movmatrix).  One
 // CTA / SM with a dedicated epilogue buffer, so the producer streams across segment
 // boundaries; each segment's Q rows are bulk-copied into a double-buffered padded slot.
+#ifndef MD_EXP_NOMATH
+#define MD_EXP_NOMATH 0  // experiment (A/B builds only): the keys kernel skips its tile math
+#endif
 template <int D, int KS, int CTAS>
 struct KeysCfg {
   static constexpr int NC = KS;
@@ -1068,7 +1110,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   }
   Seg sg;
   trace_stamp(p, 2);
-  if (p.kn != nullptr && warp < NC) {  // fused append: the new rows of this CTA's tiles
+  if (p.kn != nullptr && !p.unit_dyn && warp < NC) {  // fused append: the new rows of this CTA's tiles
     int64_t S0, E0;
     cta_range(p, pre, pl, chunk, S0, E0);
     append_own_rows<D>(p, pre, S0, E0, threadIdx.x, NC * 32);
@@ -1089,16 +1131,19 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     // Dynamic chunks are claimed one ahead (the atomic's latency hides behind a whole chunk
     // of TMA issue); when the current chunk is exhausted the claimed id (-1: none left) is
     // handed to the consumers.
+    // The dynamic-unit plan claims only when the walker runs dry (the ring's buffered stages hide
+    // the atomic), so a unit goes to whichever CTA frees up first.
     int ahead = 0;
-    if (pl.nch > pl.G && lane == 0) ahead = atomicAdd(p.dyn, 1);
+    if (pl.nch > pl.G && lane == 0 && !p.unit_dyn) ahead = atomicAdd(p.dyn, 1);
     auto next_seg = [&]() -> bool {
       while (!walk.next(p, pre, sg)) {
         if (pl.nch == pl.G) return false;
         int nxt = -1;
         if (lane == 0) {
+          if (p.unit_dyn) ahead = atomicAdd(p.dyn, 1);
           const int c = pl.G + ahead;
           nxt = c < pl.nch ? c : -1;
-          if (nxt >= 0) ahead = atomicAdd(p.dyn, 1);
+          if (nxt >= 0 && !p.unit_dyn) ahead = atomicAdd(p.dyn, 1);
           const int cs = ck & 1;
           mbar_wait(&cempty[cs], ((ck >> 1) & 1) ^ 1);
           cids[cs] = nxt;
@@ -1108,7 +1153,11 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         ++ck;
         if (nxt < 0) return false;
         chunk = nxt;
-        walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+        {
+          int64_t S_, E_;
+          cta_range(p, pre, pl, chunk, S_, E_);
+          walk.init(p, pre, S_, E_);
+        }
       }
       return true;
     };
@@ -1123,7 +1172,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       }
       __syncwarp();
       produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol, sg.n,
-                                 p.kn != nullptr ? apb : nullptr);
+                                 (p.kn != nullptr && !p.unit_dyn) ? apb : nullptr);
       ++qi;
     }
     if (lane == 0) trace_put(p, 10, globaltimer());
@@ -1147,7 +1196,11 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       ++ck;
       if (nxt < 0) return false;
       chunk = nxt;
-      walk.init(p, pre, pl.start(chunk), pl.start(chunk + 1));
+      {
+        int64_t S_, E_;
+        cta_range(p, pre, pl, chunk, S_, E_);
+        walk.init(p, pre, S_, E_);
+      }
     }
     return true;
   };
@@ -1188,7 +1241,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         if (it == 0) trace_stamp(p, 3);
         const int nvalid = min(TK, re - pos);
         const int kw0 = ks * KW;
-        if (kw0 < nvalid) {
+        if (!MD_EXP_NOMATH && kw0 < nvalid) {
           const uint32_t kt = ring + stage * C::STAGE;
           const uint32_t vt = kt + C::TILE;
           // ---------------- S^T = K Q^T : KB blocks of 16 keys x 8 query rows
@@ -1421,6 +1474,9 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int DYN_K = 4;
 constexpr int DYN_MIN_TILES = 128;  // dynamic only when a call has >= 128 tiles (8 MB of K+V) per CTA
 constexpr int DYN_STATIC_PERMILLE = 750;
+#ifndef MD_DRAFT_DYN_UNITS
+#define MD_DRAFT_DYN_UNITS 0  // StreamingLLM draft calls: dynamic whole-unit claims (A/B)
+#endif
 #ifndef MD_UNIT_ALIGNED_DRAFT
 #define MD_UNIT_ALIGNED_DRAFT 1  // draft calls: whole units per CTA (0: the stream-K plan; A/B builds only)
 #endif
@@ -1611,7 +1667,7 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   // target point (B = 64, 512 units of 1024 keys): 51.4 -> 49.1 us per call; Qwen2.5 (256 units of
   // 2048 keys): 50.7 -> 48.5 us (tools/draft_ab.py, profiles/draft_ab_r02.txt).  Not when the
   // keys kernel's dynamic tail engages (long calls), nor for the deterministic plan.
-  bool unit_aligned = false;
+  bool unit_aligned = false, unit_dyn = false;
   if ((mode == MODE_DRAFT || mode == MODE_INDEXED) && !tcg && ix.det_split_tiles == 0 && MD_UNIT_ALIGNED_DRAFT) {
     const int64_t keys_ub = mode == MODE_DRAFT ? std::min<int64_t>((int64_t)sink + window, c->capacity) : c->capacity;
     const int64_t tiles_ub = (int64_t)c->batch * c->num_kv_heads * ((keys_ub + TK - 1) / TK);
@@ -1620,8 +1676,13 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
 #ifndef MD_EXP_UNIT_FULLGRID
 #define MD_EXP_UNIT_FULLGRID 0  // experiment (A/B builds only): keep the full grid, boundaries snapped
 #endif
-      if (!MD_EXP_UNIT_FULLGRID) grid = (units_ + per - 1) / per;
-      unit_aligned = true;
+      if (MD_DRAFT_DYN_UNITS && mode == MODE_DRAFT && use_keys_kernel(R) && c->batch <= TABLE_B) {
+        grid = std::min(grid, units_);  // one unit per CTA, then claimed units
+        unit_dyn = true;
+      } else {
+        if (!MD_EXP_UNIT_FULLGRID) grid = (units_ + per - 1) / per;
+        unit_aligned = true;
+      }
     }
   }
   const int det_maxp = ix.det_split_tiles > 0
@@ -1703,7 +1764,8 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.det_split = ix.det_split_tiles;
   p.det_maxp = det_maxp;
   p.unit_aligned = unit_aligned ? 1 : 0;
-  if (unit_aligned) p.dyn_k = 0;
+  p.unit_dyn = unit_dyn ? 1 : 0;
+  if (unit_aligned || unit_dyn) p.dyn_k = 0;
   if (p.det_split > 0) p.dyn_k = 0;
   const size_t slots = partial_slots(grid, units, R, det_maxp);
   uint8_t* w = static_cast<uint8_t*>(ws);
