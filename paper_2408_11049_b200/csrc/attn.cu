@@ -462,18 +462,25 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
   constexpr int SUB = D / 64, TILE = TK * D * 2, STAGE = 2 * TILE;
   const int lane = threadIdx.x & 31;
   const bool gathered0 = (p.mode == MODE_INDEXED);
-  // MODE_INDEXED: the listed rows are copied by all 32 producer lanes with 16-byte cp.async
-  // (lane l: tile rows 2l and 2l + 1, written in the SWIZZLE_128B layout the consumers read),
-  // completing on the stage's mbarrier through cp.async.mbarrier.arrive.  (TMA tile::gather4
-  // capped this path at ~3.3 TB/s whatever the index locality; tools/gather_probe.py.)  Each
-  // lane's two row indices of the NEXT tile are loaded while the current tile is issued.
+  // MODE_INDEXED: the listed rows are copied by all 32 producer lanes with 16-byte cp.async into
+  // the SWIZZLE_128B layout the consumers read, completing on the stage's mbarrier through
+  // cp.async.mbarrier.arrive.  Lane l owns tile rows 8j + l/4 (j = 0..7) and, of each, the 16-byte
+  // chunks 4k + l%4 (k < D/32): one warp instruction moves 64 contiguous bytes of each of 8 rows,
+  // and each lane forms one K and one V row address per owned row, the chunks following as
+  // immediate offsets.  (Lane-per-row copies -- 32 rows per instruction -- ran at 3.5 TB/s, TMA
+  // tile::gather4 at 3.3; tools/gather_probe.py, tools/microbench/gather_sol.cu.)  Each lane's
+  // row indices of the NEXT tile are loaded while the current tile is issued.
+  constexpr int JR = 8, CPL = D / 32;  // rows per lane and tile, chunks per lane and row
   const int32_t* ip = gathered0 ? p.idx + ((int64_t)b * p.Hkv + kvh) * p.idx_stride : nullptr;
   const int64_t ubase = (int64_t)b * p.row_sB + (int64_t)kvh * p.row_sH;
+  const int g8 = lane >> 2, l4 = lane & 3;
   auto load_rows = [&](int pos, int nvalid, int* row) {
 #pragma unroll
-    for (int u = 0; u < 2; ++u) row[u] = (2 * lane + u < nvalid) ? __ldg(ip + pos + 2 * lane + u) : -1;
+    for (int j = 0; j < JR; ++j) row[j] = (8 * j + g8 < nvalid) ? __ldg(ip + pos + 8 * j + g8) : -1;
   };
-  int rows_next[2] = {-1, -1};
+  int rows_next[JR];
+#pragma unroll
+  for (int j = 0; j < JR; ++j) rows_next[j] = -1;
   if (gathered0 && rg.s0 < rg.e0) load_rows(rg.s0, min(TK, rg.e0 - rg.s0), rows_next);
 #pragma unroll 1
   for (int part = 0; part < 2; ++part) {
@@ -485,27 +492,28 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
       uint8_t* kt = ring + stage * STAGE;
       uint8_t* vt = kt + TILE;
       if (part == 0 && gathered0) {
-        const int row[2] = {rows_next[0], rows_next[1]};
+        int row[JR];
+#pragma unroll
+        for (int j = 0; j < JR; ++j) row[j] = rows_next[j];
         const int npos = pos + TK;
         if (npos < re) load_rows(npos, min(TK, re - npos), rows_next);
         if (lane == 0) mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
         __syncwarp();
-        const uint32_t kt_a = smem_u32(kt), vt_a = smem_u32(vt);
+        const uint32_t kt_a = smem_u32(kt) + g8 * 128, vt_a = smem_u32(vt) + g8 * 128;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (row[u] < 0) continue;  // rows past the tile's valid keys stay stale (masked / zeroed)
-          const int r = 2 * lane + u;
-          const int64_t off = (ubase + (int64_t)row[u] * p.row_sS) * D;
-          const uint16_t* ks = p.kc + off;
-          const uint16_t* vs = p.vc + off;
-          if (p.kn != nullptr && row[u] >= n - p.T) {  // fused append: a new row, from k_new / v_new
-            const int64_t src = (((int64_t)b * p.T + (row[u] - (n - p.T))) * p.Hkv + kvh) * D;
+        for (int j = 0; j < JR; ++j) {
+          if (row[j] < 0) continue;  // rows past the tile's valid keys stay stale (masked / zeroed)
+          const uint16_t* ks = p.kc + (ubase + (int64_t)row[j] * p.row_sS) * D;
+          const uint16_t* vs = p.vc + (ubase + (int64_t)row[j] * p.row_sS) * D;
+          if (p.kn != nullptr && row[j] >= n - p.T) {  // fused append: a new row, from k_new / v_new
+            const int64_t src = (((int64_t)b * p.T + (row[j] - (n - p.T))) * p.Hkv + kvh) * D;
             ks = p.kn + src;
             vs = p.vn + src;
           }
 #pragma unroll
-          for (int c = 0; c < D / 8; ++c) {
-            const uint32_t dst = (uint32_t)((c >> 3) * TK * 128 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+          for (int k = 0; k < CPL; ++k) {
+            const int c = 4 * k + l4;  // chunk; the tile row is 8j + g8, so (row & 7) == g8
+            const uint32_t dst = (uint32_t)((c >> 3) * TK * 128 + j * 1024 + (((c & 7) ^ g8) << 4));
             cp_async16_pol(kt_a + dst, ks + c * 8, pol);
             cp_async16_pol(vt_a + dst, vs + c * 8, pol);
           }
