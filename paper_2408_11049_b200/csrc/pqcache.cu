@@ -8,7 +8,8 @@
 //   pq_encode_kernel  (prefill / lazily for rows leaving the window) code[j][m] = nearest of
 //                     256 centroids of sub-space m, fp32 distance left to right, no FMA;
 //   pq_lut_kernel     the group's query heads folded into one table lut[16][256] (fp32,
-//                     no FMA), scaled by 2^e (max |lut| < 2^26) and rounded to int32;
+//                     no FMA), one CTA per (unit, 4 sub-spaces), plus their max |lut|;
+//                     the score kernel scales it by 2^e (max |lut| < 2^26) and rounds to int32;
 //   pq_score_kernel   score[j] = sum_m lutq[m][code[j][m]]: one 16-byte code per key and
 //                     thread, 16 table lookups from shared memory laid out so the 32 lanes
 //                     of a warp always hit 32 different banks (lane l reads sub-space
@@ -23,6 +24,7 @@
 // the index lists equal the oracle's bit for bit (oracle/pqcache.py P1-P5).
 #include <cuda.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "md_common.cuh"
@@ -120,73 +122,74 @@ __global__ void __launch_bounds__(256) pq_encode_kernel(const uint16_t* __restri
   }
 }
 
-// ------------------------------------------------------------------ P2 + P3 lookup table
-// grid units, 256 threads: thread c computes lut[m][c] for all 16 m.
+// ------------------------------------------------------------------ P2 lookup table
+// grid (units, 4 groups of 4 sub-spaces), 256 threads: thread c computes lut[m][c] for the
+// group's 4 sub-spaces m, each = sum over the query heads hh and dims i of
+// q[hh][m*S + i] * cent[m][c][i] (fp32, no FMA, hh outer / i inner; the 4 chains are
+// independent), and the CTA's max |lut| goes to lutmax[unit][group].  P3 (the power-of-two
+// scaling to int32) needs the max over all 16 sub-spaces, so it is applied by the score kernel
+// when it loads the table.
+constexpr int LUT_MG = 4;  // sub-spaces per LUT CTA
 template <int S>
-__global__ void __launch_bounds__(256, 4) pq_lut_kernel(const uint16_t* __restrict__ q, int Hq, int Hkv,
-                                                     const uint16_t* __restrict__ cb, int32_t* __restrict__ lutq,
-                                                     uint32_t* __restrict__ hist) {
+__global__ void __launch_bounds__(256) pq_lut_kernel(const uint16_t* __restrict__ q, int Hq, int Hkv,
+                                                     const uint16_t* __restrict__ cb, float* __restrict__ lutf,
+                                                     float* __restrict__ lutmax, uint32_t* __restrict__ hist) {
   constexpr int D = S * M;
-  extern __shared__ float qs[];  // [g][D]
+  __shared__ float qs[16 * LUT_MG * S];  // [g <= 16][LUT_MG * S]: the group's query slices of these sub-spaces
   __shared__ float red[8];
   pdl_trigger();
   pdl_wait();
-  const int unit = blockIdx.x, g = Hq / Hkv;
+  const int unit = blockIdx.x, m0 = blockIdx.y * LUT_MG, g = Hq / Hkv;
   const int b = unit / Hkv, u = unit - b * Hkv;
-  const uint16_t* qg = q + ((size_t)b * Hq + (size_t)u * g) * D;
-  for (int i = threadIdx.x; i < g * D; i += blockDim.x) qs[i] = bf16_to_f32(qg[i]);
-  __syncthreads();
   const int c = threadIdx.x;
-  const uint16_t* cbu = cb + (size_t)unit * M * NC * S;
-  float lut[M];
-  float mx = 0.f;
-  // all 16 centroid rows of this thread up front (16-byte loads, independent)
-  uint32_t cw[M][S / 2];
+  // all LUT_MG centroid rows of this thread up front (independent 16 / 8-byte loads)
+  uint32_t cw[LUT_MG][S / 2];
 #pragma unroll
-  for (int m = 0; m < M; ++m) {
-    const uint16_t* src = cbu + ((size_t)m * NC + c) * S;
+  for (int mm = 0; mm < LUT_MG; ++mm) {
+    const uint16_t* src = cb + (((size_t)unit * M + m0 + mm) * NC + c) * S;
     if constexpr (S == 8) {
       const uint4 w = __ldg(reinterpret_cast<const uint4*>(src));
-      cw[m][0] = w.x; cw[m][1] = w.y; cw[m][2] = w.z; cw[m][3] = w.w;
+      cw[mm][0] = w.x; cw[mm][1] = w.y; cw[mm][2] = w.z; cw[mm][3] = w.w;
     } else {
       const uint2 w = __ldg(reinterpret_cast<const uint2*>(src));
-      cw[m][0] = w.x; cw[m][1] = w.y;
+      cw[mm][0] = w.x; cw[mm][1] = w.y;
     }
   }
+  const uint16_t* qg = q + ((size_t)b * Hq + (size_t)u * g) * D + m0 * S;
+  for (int i = threadIdx.x; i < g * LUT_MG * S; i += blockDim.x)
+    qs[i] = bf16_to_f32(qg[(i / (LUT_MG * S)) * D + i % (LUT_MG * S)]);
+  __syncthreads();
+  float acc[LUT_MG];
 #pragma unroll
-  for (int m = 0; m < M; ++m) {
-    float cen[S];
+  for (int mm = 0; mm < LUT_MG; ++mm) acc[mm] = 0.f;
+  for (int hh = 0; hh < g; ++hh) {
 #pragma unroll
-    for (int i = 0; i < S / 2; ++i) {
-      cen[2 * i] = __uint_as_float(cw[m][i] << 16);
-      cen[2 * i + 1] = __uint_as_float(cw[m][i] & 0xffff0000u);
+    for (int mm = 0; mm < LUT_MG; ++mm) {
+#pragma unroll
+      for (int i = 0; i < S / 2; ++i) {
+        const float c0 = __uint_as_float(cw[mm][i] << 16), c1 = __uint_as_float(cw[mm][i] & 0xffff0000u);
+        acc[mm] = __fadd_rn(acc[mm], __fmul_rn(qs[hh * LUT_MG * S + mm * S + 2 * i], c0));
+        acc[mm] = __fadd_rn(acc[mm], __fmul_rn(qs[hh * LUT_MG * S + mm * S + 2 * i + 1], c1));
+      }
     }
-    float acc = 0.f;
-    for (int hh = 0; hh < g; ++hh) {
+  }
+  float mx = 0.f;
 #pragma unroll
-      for (int i = 0; i < S; ++i) acc = __fadd_rn(acc, __fmul_rn(qs[hh * D + m * S + i], cen[i]));
-    }
-    lut[m] = acc;
-    mx = fmaxf(mx, fabsf(acc));
+  for (int mm = 0; mm < LUT_MG; ++mm) {
+    lutf[((size_t)unit * NC + c) * M + m0 + mm] = acc[mm];  // [c][m]
+    mx = fmaxf(mx, fabsf(acc[mm]));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
   __syncthreads();
-  mx = red[0];
-#pragma unroll
-  for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
-  int e = 0;
-  if (mx > 0.f) {
-    int E;
-    frexpf(mx, &E);
-    e = 26 - E;
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+    lutmax[(size_t)unit * (M / LUT_MG) + blockIdx.y] = fmaxf(red[0], mx);
   }
-  int32_t* dst = lutq + (size_t)unit * M * NC;
-#pragma unroll
-  for (int m = 0; m < M; ++m) dst[c * M + m] = __float2int_rn(ldexpf(lut[m], e));  // [c][m]
   // the unit's pass-1 histogram, accumulated by the score kernel
-  for (int i = threadIdx.x; i < HIST1; i += blockDim.x) hist[(size_t)unit * HIST1 + i] = 0u;
+  if (blockIdx.y == 0)
+    for (int i = threadIdx.x; i < HIST1; i += blockDim.x) hist[(size_t)unit * HIST1 + i] = 0u;
 }
 
 // ------------------------------------------------------------------ P4 scores
@@ -197,7 +200,8 @@ __device__ __forceinline__ uint32_t okey(int32_t v) { return static_cast<uint32_
 // densely (candidate j - s0) and the top digit (bits 31..22 of the order-preserving key) of
 // every score is counted into the unit's global histogram.
 __global__ void __launch_bounds__(SCORE_THREADS, 2) pq_score_kernel(const uint8_t* __restrict__ codes, int code_cap,
-                                                                 const int32_t* __restrict__ lutq,
+                                                                 const float* __restrict__ lutf,
+                                                                 const float* __restrict__ lutmax,
                                                                  const int32_t* __restrict__ kv_len, int Hkv, int sink,
                                                                  int window, int32_t* __restrict__ scores,
                                                                  int score_stride, uint32_t* __restrict__ hist_g) {
@@ -213,10 +217,20 @@ __global__ void __launch_bounds__(SCORE_THREADS, 2) pq_score_kernel(const uint8_
   const int s0 = min(sink, n), tail = max(s0, n - window);
   const int lo = s0 + (int)blockIdx.y * SCORE_CH, hi = min(tail, lo + SCORE_CH);
   if (lo >= hi) return;  // uniform
-  const int32_t* src = lutq + (size_t)unit * M * NC;
-  for (int i = threadIdx.x; i < M * NC; i += SCORE_THREADS) {  // lutq is [c][m]: coalesced, <= 2-way stores
+  // P3: scale by 2^e with max |lut| < 2^26 (e from the max over the 16 sub-spaces) and round
+  float mx = 0.f;
+#pragma unroll
+  for (int k = 0; k < M / LUT_MG; ++k) mx = fmaxf(mx, __ldg(lutmax + (size_t)unit * (M / LUT_MG) + k));
+  int e = 0;
+  if (mx > 0.f) {
+    int E;
+    frexpf(mx, &E);
+    e = 26 - E;
+  }
+  const float* src = lutf + (size_t)unit * M * NC;
+  for (int i = threadIdx.x; i < M * NC; i += SCORE_THREADS) {  // lutf is [c][m]: coalesced, <= 2-way stores
     const int c = i >> 4, m = i & 15;
-    const int32_t v = __ldg(src + i);
+    const int32_t v = __float2int_rn(ldexpf(__ldg(src + i), e));
     tab[c * 64 + m] = v;
     tab[c * 64 + 16 + m] = v;
   }
@@ -242,14 +256,11 @@ __global__ void __launch_bounds__(SCORE_THREADS, 2) pq_score_kernel(const uint8_
   const char* tabc = reinterpret_cast<const char*>(tab);
   const uint4* crow = reinterpret_cast<const uint4*>(codes + (size_t)unit * code_cap * M);
   int32_t* out = scores + (size_t)unit * score_stride - s0;
-  // the 4 code words of a slot read in the order w'[i] = w[i ^ qx] (per-lane byte offsets)
-  uint32_t woff[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) woff[i] = (uint32_t)((i ^ qx) << 2);
-  auto score_one = [&](uint32_t slot) -> int32_t {
-    uint32_t w[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w[i]) : "r"(slot + woff[i]));
+  // the 16-byte code's words are put in the order w'[i] = w[i ^ qx] with two levels of selects
+  const bool sw1 = qx & 1, sw2 = qx & 2;
+  auto score_one = [&](const uint4 v) -> int32_t {
+    const uint32_t a0 = sw1 ? v.y : v.x, a1 = sw1 ? v.x : v.y, a2 = sw1 ? v.w : v.z, a3 = sw1 ? v.z : v.w;
+    const uint32_t w[4] = {sw2 ? a2 : a0, sw2 ? a3 : a1, sw2 ? a0 : a2, sw2 ? a1 : a3};
     int32_t acc = 0;
 #pragma unroll
     for (int i = 0; i < M; ++i) acc += *reinterpret_cast<const int32_t*>(tabc + __byte_perm(w[i >> 2], xo[i >> 1], sel[i & 3]));
@@ -260,7 +271,8 @@ __global__ void __launch_bounds__(SCORE_THREADS, 2) pq_score_kernel(const uint8_
     atomicAdd(&hist[okey(sc) >> 22], 1u);
   };
   // per-thread NS-deep cp.async pipeline: the codes of this thread's next NS - 1 keys are in
-  // flight while it scores the current one (each thread reads only the slots it filled)
+  // flight while it scores the current one (each thread reads only the slots it filled; a
+  // warp's 128-bit reads of its slots are 512 contiguous bytes: 4 conflict-free wavefronts)
   const uint32_t ring = smem_u32(hist + HIST1) + threadIdx.x * 16;
   const int j0 = lo + threadIdx.x;
   const int nk = j0 < hi ? (hi - j0 + SCORE_THREADS - 1) / SCORE_THREADS : 0;
@@ -274,7 +286,7 @@ __global__ void __launch_bounds__(SCORE_THREADS, 2) pq_score_kernel(const uint8_
     if (i + NS - 1 < nk) cp_async16(ring + wr * SCORE_THREADS * 16, crow + j0 + (i + NS - 1) * SCORE_THREADS);
     cp_async_commit();
     cp_async_wait<NS - 1>();
-    emit(j0 + i * SCORE_THREADS, score_one(ring + rd * SCORE_THREADS * 16));
+    emit(j0 + i * SCORE_THREADS, score_one(lds128(ring + rd * SCORE_THREADS * 16)));
     rd = rd == NS - 1 ? 0 : rd + 1;
     wr = wr == NS - 1 ? 0 : wr + 1;
   }
@@ -528,7 +540,7 @@ static size_t pq_align(size_t x) { return (x + 255) & ~size_t(255); }
 static int pq_score_stride(int maxL) { return (maxL + 3) & ~3; }
 static size_t pq_ws(int B, int Hkv, int maxL) {
   const size_t units = (size_t)B * Hkv;
-  return pq_align(units * pq::M * pq::NC * 4) + pq_align(units * pq::HIST1 * 4) +
+  return pq_align(units * pq::M * pq::NC * 4) + pq_align(units * pq::M * 4) + pq_align(units * pq::HIST1 * 4) +
          pq_align(units * (size_t)pq_score_stride(maxL) * 4);
 }
 
@@ -592,8 +604,10 @@ extern "C" MD_API md_status md_pq_select(const void* q, int32_t batch, int32_t n
              "md_pq_select: workspace of %zu bytes required, %zu given", need, workspace_bytes);
   const int units = batch * num_kv_heads;
   uint8_t* w8 = static_cast<uint8_t*>(workspace);
-  auto* lutq = reinterpret_cast<int32_t*>(w8);
+  auto* lutf = reinterpret_cast<float*>(w8);
   w8 += pq_align((size_t)units * pq::M * pq::NC * 4);
+  auto* lutmax = reinterpret_cast<float*>(w8);
+  w8 += pq_align((size_t)units * pq::M * 4);
   auto* hist = reinterpret_cast<uint32_t*>(w8);
   w8 += pq_align((size_t)units * pq::HIST1 * 4);
   auto* scores = reinterpret_cast<int32_t*>(w8);
@@ -602,13 +616,13 @@ extern "C" MD_API md_status md_pq_select(const void* q, int32_t batch, int32_t n
   const auto* cb = static_cast<const uint16_t*>(codebook);
   cudaStream_t s = (cudaStream_t)stream;
   const int g = num_q_heads / num_kv_heads;
-  const size_t lut_smem = (size_t)g * head_dim * 4;
+  (void)g;
   if (head_dim == 128)
-    launch_pdl(pq::pq_lut_kernel<8>, dim3(units), dim3(256), lut_smem, s, qq, (int)num_q_heads, (int)num_kv_heads,
-               cb, lutq, hist);
+    launch_pdl(pq::pq_lut_kernel<8>, dim3(units, pq::M / pq::LUT_MG), dim3(256), 0, s, qq, (int)num_q_heads, (int)num_kv_heads, cb,
+               lutf, lutmax, hist);
   else
-    launch_pdl(pq::pq_lut_kernel<4>, dim3(units), dim3(256), lut_smem, s, qq, (int)num_q_heads, (int)num_kv_heads,
-               cb, lutq, hist);
+    launch_pdl(pq::pq_lut_kernel<4>, dim3(units, pq::M / pq::LUT_MG), dim3(256), 0, s, qq, (int)num_q_heads, (int)num_kv_heads, cb,
+               lutf, lutmax, hist);
   if (md_status st = check_launch("pq_lut_kernel"); st != MD_OK) return st;
   static int done_dev = -1;  // per-process; the attribute call is idempotent (benign race)
   int dev = 0;
@@ -621,9 +635,13 @@ extern "C" MD_API md_status md_pq_select(const void* q, int32_t batch, int32_t n
       return check_launch("cudaFuncSetAttribute");
     done_dev = dev;
   }
-  const unsigned chunks = (unsigned)((max_kv_len + pq::SCORE_CH - 1) / pq::SCORE_CH);
+  // candidates of a unit: [s0, tail) with tail <= max(s0, n - window), so at most
+  // max(1, max_kv_len - window) of them (a chunk past every unit's candidates would only load
+  // the table: 3 chunks instead of 2 at the 32k BASELINE shapes)
+  const int max_cand = std::max(1, (int)max_kv_len - (int)window);
+  const unsigned chunks = (unsigned)((max_cand + pq::SCORE_CH - 1) / pq::SCORE_CH);
   launch_pdl(pq::pq_score_kernel, dim3(units, chunks), dim3(pq::SCORE_THREADS), (size_t)pq::SCORE_SMEM, s, codes,
-             (int)code_capacity, (const int32_t*)lutq, kv_len, (int)num_kv_heads, (int)sink, (int)window, scores,
+             (int)code_capacity, (const float*)lutf, (const float*)lutmax, kv_len, (int)num_kv_heads, (int)sink, (int)window, scores,
              sstride, hist);
   if (md_status st = check_launch("pq_score_kernel"); st != MD_OK) return st;
   launch_pdl(pq::pq_select_kernel, dim3(units), dim3(pq::SEL_THREADS), (size_t)pq::SEL_SMEM, s, (const int32_t*)scores, sstride,
