@@ -41,11 +41,14 @@ constexpr int SMEM_MAX = 232448;             // 227 KB per CTA
 // over the same 128 TMEM lanes (warp w reads lane quadrant w % 4), which walk their columns in
 // chunks of CH = 32 (or 16) in two passes per stage (max test, then exponentials), so a thread
 // keeps only its CW row sums and one chunk of scores.
+#ifndef MD_TC_CH16
+#define MD_TC_CH16 0  // A/B: 16-column TMEM chunks for every row-group width
+#endif
 template <int NP>
 struct Cfg {
   static constexpr int NG = NP <= 48 ? 1 : 2;        // row groups
   static constexpr int CW = NP / NG;                 // query-row columns per group
-  static constexpr int CH = CW == 32 ? 32 : 16;      // columns per TMEM load chunk (NG > 1)
+  static constexpr int CH = (CW == 32 && !MD_TC_CH16) ? 32 : 16;  // columns per TMEM load chunk (NG > 1)
   static constexpr int SM_THREADS = 128 * NG;        // softmax / epilogue threads
   static constexpr int THREADS = SM_THREADS + 64;    // + producer warp + MMA warp
   static constexpr int NQ = NP <= 32 ? 2 : 1;        // Q buffers (by segment parity)
