@@ -234,7 +234,14 @@ struct Seg {
 struct SegWalker {
   int64_t t, end, ustart;
   int b, h, tiles_b;
+  int umode;  // 1: whole units t .. end-1 by unit index (unit-aligned plan; no prefix table)
+  __device__ void init_units(int u0, int u1) {
+    umode = 1;
+    t = u0;
+    end = u1;
+  }
   __device__ void init(const AttnParams& p, const int* pre, int64_t S, int64_t E) {
+    umode = 0;
     t = S;
     end = E;
     int64_t acc = 0;
@@ -263,6 +270,21 @@ struct SegWalker {
     ustart = acc + (int64_t)h * tiles_b;
   }
   __device__ bool next(const AttnParams& p, const int* pre, Seg& sg) {
+    if (umode) {  // the next unit with at least one key tile
+      while (t < end) {
+        const int u = static_cast<int>(t++);
+        sg.b = u / p.Hkv;
+        sg.kvh = u - sg.b * p.Hkv;
+        sg.unit = u;
+        sg.n = __ldg(p.kv_len + sg.b);
+        sg.tiles = (unit_keys(p, sg.n, sg.b) + TK - 1) / TK;
+        sg.lo = 0;
+        sg.hi = sg.tiles;
+        sg.ustart = 0;  // whole units need no partial slot
+        if (sg.tiles > 0) return true;
+      }
+      return false;
+    }
     if (t >= end) return false;
     sg.b = b;
     sg.kvh = h;
@@ -375,10 +397,8 @@ __device__ __forceinline__ bool tile_has_new(const AttnParams& p, int n, int pos
   return p.kn != nullptr && pos < n && pos + nvalid > n - p.T;
 }
 template <int D>
-__device__ void append_own_rows(const AttnParams& p, const int* pre, int64_t S, int64_t E, int tid, int nthr) {
+__device__ void append_own_rows(const AttnParams& p, const int* pre, SegWalker w, int tid, int nthr) {
   constexpr int NV = D / 8;  // 16-byte vectors per row
-  SegWalker w;
-  w.init(p, pre, S, E);
   Seg sg;
   while (w.next(p, pre, sg)) {
     const Ranges rg = seg_ranges(p, sg);
@@ -1020,6 +1040,9 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
 // P^T operand is the bf16-packed S^T fragment transposed in registers (movmatrix).  One
 // CTA / SM with a dedicated epilogue buffer, so the producer streams across segment
 // boundaries; each segment's Q rows are bulk-copied into a double-buffered padded slot.
+#ifndef MD_DIRECT_UNITS
+#define MD_DIRECT_UNITS 1  // unit-aligned keys-kernel calls walk their units without a prefix table (0: A/B builds)
+#endif
 #ifndef MD_EXP_NOMATH
 #define MD_EXP_NOMATH 0  // experiment (A/B builds only): the keys kernel skips its tile math
 #endif
@@ -1102,26 +1125,45 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   if (p.pdl_early) pdl_trigger();  // else the dependent launch waits for this grid's exit
   pdl_wait();  // kv_len, the cache and q may come from the previous kernel
   trace_stamp(p, 1);
-  __syncthreads();
-  build_prefix(p, pre);
-  // the plan lives in shared memory (read only at segment boundaries: keeps registers free)
-  if (threadIdx.x == 0) *plan_smem = make_plan(p, total_tiles(p, pre), gridDim.x);
+  // Unit-aligned plan (draft calls): CTA c owns the whole units [c*U/G, (c+1)*U/G), G = gridDim.x,
+  // so it needs neither the per-sequence prefix table nor a plan -- its producer issues the
+  // first tile right after reading its first unit's kv_len (MD_DIRECT_UNITS; the prefix walk
+  // costs a batch-wide kv_len load, a scan and two CTA barriers before the first TMA issue)
+  const bool direct = MD_DIRECT_UNITS && p.unit_aligned;
+  if (direct) {
+    if (threadIdx.x == 0) {
+      Plan d{};
+      d.G = d.nch = gridDim.x;
+      *plan_smem = d;
+    }
+  } else {
+    __syncthreads();
+    build_prefix(p, pre);
+    // the plan lives in shared memory (read only at segment boundaries: keeps registers free)
+    if (threadIdx.x == 0) *plan_smem = make_plan(p, total_tiles(p, pre), gridDim.x);
+  }
   __syncthreads();
   const Plan& pl = *plan_smem;
   if ((int)blockIdx.x >= pl.G) return;  // uniform across the CTA
   int chunk = blockIdx.x;                // this CTA's static chunk, then claimed dynamic ones
+  const int U = p.B * p.Hkv;
+  auto init_walk = [&](SegWalker& w) {
+    if (direct) {
+      w.init_units((int)((int64_t)chunk * U / pl.G), (int)((int64_t)(chunk + 1) * U / pl.G));
+    } else {
+      int64_t S0, E0;
+      cta_range(p, pre, pl, chunk, S0, E0);
+      w.init(p, pre, S0, E0);
+    }
+  };
   SegWalker walk;
-  {
-    int64_t S0, E0;
-    cta_range(p, pre, pl, chunk, S0, E0);
-    walk.init(p, pre, S0, E0);
-  }
+  init_walk(walk);
   Seg sg;
   trace_stamp(p, 2);
   if (p.kn != nullptr && !p.unit_dyn && warp < NC) {  // fused append: the new rows of this CTA's tiles
-    int64_t S0, E0;
-    cta_range(p, pre, pl, chunk, S0, E0);
-    append_own_rows<D>(p, pre, S0, E0, threadIdx.x, NC * 32);
+    SegWalker aw;
+    init_walk(aw);
+    append_own_rows<D>(p, pre, aw, threadIdx.x, NC * 32);
     __syncwarp();
     if (lane == 0) mbar_arrive(apb);
   }

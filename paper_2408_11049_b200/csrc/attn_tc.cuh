@@ -288,7 +288,9 @@ __global__ void __launch_bounds__(Cfg<NP>::THREADS, 1)
   if (p.kn != nullptr && warp < 4 && active) {  // fused append: the new rows of this CTA's tiles
     int64_t S0, E0;
     cta_range(p, pre, pl, chunk, S0, E0);
-    append_own_rows<128>(p, pre, S0, E0, threadIdx.x, 128);
+    SegWalker aw;
+    aw.init(p, pre, S0, E0);
+    append_own_rows<128>(p, pre, aw, threadIdx.x, 128);
     __syncwarp();
     if (lane == 0) mbar_arrive(apb);
   }

@@ -59,12 +59,18 @@ for c in range(6):
     sm = t[:, 6].astype(int)
     for s_, e_ in zip(sm, end):
         ends_by_sm.setdefault(int(s_), []).append(float(e_))
+    located = (t[:, 2] - t1) / 1e3
     row = {"ctas": int(len(t)), "start_p50": round(float(np.median(start)), 2),
+           "range_located_p50_p100": [round(float(np.percentile(located, x)), 2) for x in (50, 100)],
            "first_tile_p0_p50_p100": [round(float(np.percentile(first, x)), 2) for x in (0, 50, 100)],
            "end_p0_p10_p50_p90_p100": [round(float(np.percentile(end, x)), 2) for x in (0, 10, 50, 90, 100)],
            "end_p50_by_segments": {int(s): round(float(np.median(end[seg == s])), 2) for s in np.unique(seg)},
            "ctas_by_segments": {int(s): int((seg == s).sum()) for s in np.unique(seg)},
-           "last_epilogue_to_end_p50": round(float(np.median(end - last_epi)), 2)}
+           "last_epilogue_to_end_p50": round(float(np.median(end - last_epi)), 2),
+           "epilogue_phases_p50": {"combine": round(float(np.median(t[:, 7] - t[:, 4])) / 1e3, 2),
+                                   "stores": round(float(np.median(t[:, 8] - t[:, 7])) / 1e3, 2),
+                                   "to_end": round(float(np.median(t[:, 5] - t[:, 8])) / 1e3, 2)},
+           "producer_done_to_end_p50": round(float(np.median(t[:, 5] - t[:, 10])) / 1e3, 2)}
     res["calls"].append(row)
 # per-SM persistence: correlation of an SM's mean end time between even and odd calls
 sms = sorted(ends_by_sm)
