@@ -1,6 +1,8 @@
 """Build the sm_100a shared libraries in-tree with nvcc (no JIT cache, no torch extension).
 
   paper_2408_11049_b200/libmagicdec_b200.so   the product: csrc/*.cu behind include/magicdec_b200.h
+  paper_2408_11049_b200/libmagicdec_b200_debug.so  the same with -DMD_DEBUG: device-side
+                                              preconditions trap (tests/test_gpu_debug.py)
   synth/libmd_synth.so                        the GPU twin of the seeded input generators
 
 Run `python -m paper_2408_11049_b200.build` (or __graft_entry__.build()).  Rebuilds only
@@ -21,6 +23,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC,-fvis
          "-cudart", "static", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 LIB = os.path.join(HERE, "libmagicdec_b200.so")
+DEBUG_LIB = os.path.join(HERE, "libmagicdec_b200_debug.so")
 SYNTH_LIB = os.path.join(ROOT, "synth", "libmd_synth.so")
 
 
@@ -64,11 +67,15 @@ def _nvcc(sources, out, extra=(), log=None, force=False):
 def build(force: bool = False, verbose: bool = False) -> None:
     srcs = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
     # export only the md_* C ABI: default-visibility for the extern "C" entry points
-    built = _nvcc(srcs, LIB, extra=["-DMD_BUILD"],
-                  log=os.path.join(HERE, "build_ptxas.log"), force=force)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=2) as ex:
+        dbg = ex.submit(_nvcc, srcs, DEBUG_LIB, extra=["-DMD_BUILD", "-DMD_DEBUG"], force=force)
+        built = _nvcc(srcs, LIB, extra=["-DMD_BUILD"], log=os.path.join(HERE, "build_ptxas.log"), force=force)
+        dbuilt = dbg.result()
     sbuilt = _nvcc([os.path.join(ROOT, "synth", "csrc", "synth_gen.cu")], SYNTH_LIB, force=force)
     if verbose:
         print(f"libmagicdec_b200.so: {'built' if built else 'up to date'}; "
+              f"libmagicdec_b200_debug.so: {'built' if dbuilt else 'up to date'}; "
               f"libmd_synth.so: {'built' if sbuilt else 'up to date'}")
 
 

@@ -109,6 +109,7 @@ struct AttnParams {
   // at a time from an atomic counter (fast SMs take more units; nothing is split or merged); the
   // fused append is then done by the producer warp right before it issues a tile holding a new row
   int unit_dyn;
+  int cap;                // cache capacity (rows), for the MD_DEBUG precondition checks
 };
 
 // ------------------------------------------------------------------ stream-K decomposition
@@ -222,6 +223,16 @@ __device__ Plan make_plan(const AttnParams& p, int64_t total, int grid) {
   return pl;
 }
 
+// MD_DEBUG: the header's device preconditions on kv_len[b] (and the index-list draft's counts)
+__device__ __forceinline__ void check_len(const AttnParams& p, int b, int n) {
+  MD_DCHECK(n <= p.cap && n >= (p.mode == MODE_VERIFY ? p.T : 1));
+  if (p.mode == MODE_INDEXED) {
+    const int ts = __ldg(p.tail_start + b), ic = __ldg(p.idx_count + b);
+    MD_DCHECK(ts <= n && ic >= 0 && ic <= p.idx_stride && ic + n - ts >= 1);
+  }
+  (void)b;
+}
+
 // One contiguous piece of one unit processed by one CTA: tiles [lo, hi) of `tiles`.
 struct Seg {
   int b, kvh, unit, n, tiles, lo, hi;
@@ -277,6 +288,7 @@ struct SegWalker {
         sg.kvh = u - sg.b * p.Hkv;
         sg.unit = u;
         sg.n = __ldg(p.kv_len + sg.b);
+        check_len(p, sg.b, sg.n);
         sg.tiles = (unit_keys(p, sg.n, sg.b) + TK - 1) / TK;
         sg.lo = 0;
         sg.hi = sg.tiles;
@@ -290,6 +302,7 @@ struct SegWalker {
     sg.kvh = h;
     sg.unit = b * p.Hkv + h;
     sg.n = __ldg(p.kv_len + b);
+    check_len(p, b, sg.n);
     sg.tiles = tiles_b;
     sg.ustart = ustart;
     sg.lo = static_cast<int>(t - ustart);
@@ -1815,6 +1828,7 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.det_maxp = det_maxp;
   p.unit_aligned = unit_aligned ? 1 : 0;
   p.unit_dyn = unit_dyn ? 1 : 0;
+  p.cap = c->capacity;
   if (unit_aligned || unit_dyn) p.dyn_k = 0;
   if (p.det_split > 0) p.dyn_k = 0;
   const size_t slots = partial_slots(grid, units, R, det_maxp);

@@ -11,7 +11,7 @@ __global__ void __launch_bounds__(256) kv_append_kernel(uint16_t* __restrict__ k
                                                         const uint16_t* __restrict__ kn,
                                                         const uint16_t* __restrict__ vn,
                                                         const int32_t* __restrict__ start, int start_off, int T,
-                                                        int Hkv, int d,
+                                                        int Hkv, int d, int cap,
                                                         int64_t sB, int64_t sH, int64_t sS, int64_t nvec) {
   pdl_trigger();
   pdl_wait();
@@ -23,7 +23,9 @@ __global__ void __launch_bounds__(256) kv_append_kernel(uint16_t* __restrict__ k
     const int64_t bt = row / Hkv;
     const int t = static_cast<int>(bt % T);
     const int b = static_cast<int>(bt / T);
-    const int64_t dst = b * sB + h * sH + (int64_t)(__ldg(start + b) + start_off + t) * sS + c;
+    const int s0 = __ldg(start + b) + start_off;
+    MD_DCHECK(s0 >= 0 && s0 + T <= cap);  // rows [start, start + T) inside the cache
+    const int64_t dst = b * sB + h * sH + (int64_t)(s0 + t) * sS + c;
     const uint4 kv = __ldg(reinterpret_cast<const uint4*>(kn + row * d + c));
     const uint4 vv = __ldg(reinterpret_cast<const uint4*>(vn + row * d + c));
     *reinterpret_cast<uint4*>(kc + dst) = kv;
@@ -65,6 +67,7 @@ md_status launch_kv_append(const md_kv_cache* c, const void* k_new, const void* 
   launch_pdl(kv_append_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0, stream,
              static_cast<uint16_t*>(c->k), static_cast<uint16_t*>(c->v), static_cast<const uint16_t*>(k_new),
              static_cast<const uint16_t*>(v_new), start, start_off, (int)T, (int)c->num_kv_heads, (int)c->head_dim,
+             (int)c->capacity,
              (int64_t)c->stride_b, (int64_t)c->stride_h, (int64_t)c->stride_s, nvec);
   return check_launch("md_kv_append");
 }

@@ -7,6 +7,17 @@
 
 #define MD_DEV __device__ __forceinline__
 
+// Device-side preconditions of include/magicdec_b200.h (undefined behaviour in release builds):
+// a build with -DMD_DEBUG (libmagicdec_b200_debug.so) traps on a violation.
+#ifdef MD_DEBUG
+#define MD_DCHECK(cond) \
+  do {                  \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define MD_DCHECK(cond) ((void)0)
+#endif
+
 namespace md {
 
 // ------------------------------------------------------------------ shared-memory addresses

@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(SCORE_THREADS, 2) pq_score_kernel(const uint8_
   const int unit = blockIdx.x;
   const int b = unit / Hkv;
   const int n = __ldg(kv_len + b);
+  MD_DCHECK(n >= 0 && n <= code_cap);  // kv_len[b] <= code_capacity (every scored row is encoded)
   const int s0 = min(sink, n), tail = max(s0, n - window);
   const int lo = s0 + (int)blockIdx.y * SCORE_CH, hi = min(tail, lo + SCORE_CH);
   if (lo >= hi) return;  // uniform

@@ -247,8 +247,10 @@ __global__ void __launch_bounds__(ACC_THREADS) spec_accept_kernel(
       bool reject = false;
       if (tid < gamma) {
         const int x = __ldg(db + tid);
+        MD_DCHECK(x >= 0 && x < V);  // draft token ids < V
         const double px = __ldg(pb + (int64_t)tid * Vl + x);
         const double qx = __ldg(q + ((int64_t)b * gamma + tid) * Vl + x);
+        MD_DCHECK(px >= 0.0 && px <= 1.0 && qx >= 0.0 && qx <= 1.0);  // finite probabilities in [0, 1] (NaN fails)
         const double m = static_cast<double>(__ldg(rb + tid) >> 3);
         reject = !(m * qx < px * 536870912.0);
       }
@@ -281,6 +283,7 @@ __global__ void __launch_bounds__(ACC_THREADS) spec_accept_kernel(
     token = -1;
     for (int j = 0; j < gamma; ++j) {
       const int am = block_argmax(pb + (int64_t)j * Vl, V, sm);
+      MD_DCHECK(__ldg(db + j) >= 0 && __ldg(db + j) < V);
       if (am != __ldg(db + j)) {
         n = j;
         token = am;

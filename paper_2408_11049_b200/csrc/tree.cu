@@ -198,6 +198,10 @@ __global__ void __launch_bounds__(TR_THREADS) spec_accept_tree_kernel(
   const int32_t* par = parent + (int64_t)b * T;
   const uint32_t* rb = rnd ? rnd + (int64_t)b * (T + 1) : nullptr;
   const int chunk = (V + TR_THREADS - 1) / TR_THREADS;
+#ifdef MD_DEBUG
+  for (int c = tid; c < T; c += TR_THREADS)  // token ids < V, topological parents (parent[t] < t)
+    MD_DCHECK(__ldg(tok + c) >= 0 && __ldg(tok + c) < V && (c == 0 || (__ldg(par + c) >= 0 && __ldg(par + c) < c)));
+#endif
   int cur = 0, npath = 0, kr = 0, token = -1;
   int32_t* nodes_out = accepted_nodes ? accepted_nodes + (int64_t)b * T : nullptr;
   int32_t* out = out_tokens + (int64_t)b * T;
