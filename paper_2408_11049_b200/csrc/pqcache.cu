@@ -42,6 +42,8 @@ constexpr int SCORE_SMEM = NC * 64 * 4 + 1024 * 4 + NS * SCORE_THREADS * 16;  //
 constexpr int HIST1 = 1024;      // pass-1 digit: key bits 31..22
 constexpr int HIST2 = 2048;      // passes 2, 3: bits 21..11, 10..0
 constexpr int TIE_CAP = 2048;    // keys of the cutoff bin kept in shared memory
+// (measured: 256 threads at 4 CTAs/SM -- one wave of the 512 units -- gave 141 -> 136 us of
+// T_select at the Llama-3.1 point but 182 -> 220 us for Qwen2.5's 256 units of 100k candidates)
 constexpr int SEL_THREADS = 512;
 constexpr int RL = 36;           // candidates per select thread run (16-byte loads, no bank conflicts)
 constexpr int SB = SEL_THREADS * RL;  // candidates staged in shared memory per super-block
