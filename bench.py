@@ -175,6 +175,31 @@ def _free_port():
     return port
 
 
+def graph_time_calls(fn, n, rot):
+    """Mean device time per call of n back-to-back calls fn(0..n-1) (the caller rotates `rot`
+    physically distinct layer caches by the index), as the step runs them: captured in one CUDA
+    graph (no host launch gaps; the kernels' programmatic-dependent-launch edges are kept), one
+    warm replay, then CUDA events around 3 replays on the capture stream."""
+    import torch
+    for r in range(rot):
+        fn(r)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.stream(cs):
+        with torch.cuda.graph(g, stream=cs):
+            for r in range(n):
+                fn(r)
+        g.replay()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cs)
+        for _ in range(3):
+            g.replay()
+        b.record(cs)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / (3 * n)
+
+
 def spawn_ranks(args, argv):
     """`bench.py --gpus N` without a torchrun environment: re-launch this command under
     torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous)."""
@@ -504,18 +529,10 @@ def run_gpu(args):
     kvl_now = (committed + T).cpu().numpy()
     kv_len_v = torch.from_numpy(kvl_now.astype(np.int32)).to(dev)
     kv_len_d = torch.from_numpy((committed + 1).cpu().numpy().astype(np.int32)).to(dev)
-    nrep = max(2 * R, 8)
+    nrep = max(8 * R, 32)
 
     def time_calls(fn):
-        fn(0)
-        torch.cuda.synchronize()
-        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for r in range(nrep):
-            fn(r)
-        b_.record()
-        torch.cuda.synchronize()
-        return a.elapsed_time(b_) / nrep
+        return graph_time_calls(fn, nrep, R)
 
     # the kernels the step runs: with the fused append, the *_append calls (their algorithmic
     # bytes add the new rows read from k_new / v_new and written to the cache: 4 B*T*Hkv*d*2)
@@ -663,16 +680,8 @@ def efficiency_check(args, md, S, SC, torch, dist, dev, rank, world, per_rank, r
         ws_v = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, T, max_kv), dtype=torch.uint8, device=dev)
         ws_d = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, 1, sink + window), dtype=torch.uint8, device=dev)
 
-        def tcall(fn, n=8):
-            fn(0)
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            for i in range(n):
-                fn(i)
-            b.record()
-            torch.cuda.synchronize()
-            return a.elapsed_time(b) / n
+        def tcall(fn):
+            return graph_time_calls(fn, 16, 2)
 
         t1v = tcall(lambda i: md.verify_attn_full(qv, kc[i % 2], vc[i % 2], kv_v, max_kv, scale, ov, None, ws_v))
         t1d = tcall(lambda i: md.draft_attn_sparse(qd, kc[i % 2], vc[i % 2], kv_d, sink, window, scale, od, None,
