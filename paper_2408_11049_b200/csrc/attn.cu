@@ -1537,6 +1537,9 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int DYN_K = 4;
 constexpr int DYN_MIN_TILES = 128;  // dynamic only when a call has >= 128 tiles (8 MB of K+V) per CTA
 constexpr int DYN_STATIC_PERMILLE = 750;
+#ifndef MD_TC_MORE_RR
+#define MD_TC_MORE_RR 1  // compile-time row counts for the paper's gammas (0: A/B builds, faster compile)
+#endif
 #ifndef MD_DRAFT_DYN_UNITS
 #define MD_DRAFT_DYN_UNITS 0  // StreamingLLM draft calls: dynamic whole-unit claims (A/B)
 #endif
@@ -1852,6 +1855,19 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
     // the BASELINE shapes get a compile-time row count (Llama-3.1 g=4 x T=5, Qwen2.5 g=7 x T=5)
     st = (R == 20)   ? launch_tc<32, 20>(tm, qm, p, grid, s)
          : (R == 35) ? launch_tc<48, 35>(tm, qm, p, grid, s)
+#if MD_TC_MORE_RR
+         // the paper's other operating points: Llama-3.1-8B gamma 5 / 6 /
+         // 7 / 8 / 11 (R = 24 / 28 / 32 / 36 / 48), Mistral-7B gamma 5 (24), Qwen2.5-7B gamma 3 / 5
+         // (28 / 42): compile-time rows skip the padded columns' work (measured at 100k, B = 41:
+         // R = 36 6.40 -> 6.81 TB/s, R = 48 6.20 -> 6.60; at 32k R = 24 6.76 -> 7.05;
+         // profiles/rows_sweep_r02_compile_time_rows.txt)
+         : (R == 24) ? launch_tc<32, 24>(tm, qm, p, grid, s)
+         : (R == 28) ? launch_tc<32, 28>(tm, qm, p, grid, s)
+         : (R == 32) ? launch_tc<32, 32>(tm, qm, p, grid, s)
+         : (R == 36) ? launch_tc<48, 36>(tm, qm, p, grid, s)
+         : (R == 42) ? launch_tc<48, 42>(tm, qm, p, grid, s)
+         : (R == 48) ? launch_tc<48, 48>(tm, qm, p, grid, s)
+#endif
          : (R <= 16) ? launch_tc<16, 0>(tm, qm, p, grid, s)
          : (R <= 32) ? launch_tc<32, 0>(tm, qm, p, grid, s)
          // 32 < R <= 64 (R != 35): two row groups (measured: R = 48 at 5.9 TB/s with one group of

@@ -66,7 +66,14 @@ VERIFY_CASES = [
     ("decode_T1",      2, 32, 8, 128, 1, [300, 1]),
     ("gqa_g8_T8",      2, 16, 2, 64, 8, [130, 8]),       # 64 rows = 4 m-tiles
     ("d64_ragged",     4, 8, 2, 64, 3, [3, 65, 128, 129]),
-    ("tc_generic_24",  2, 16, 4, 128, 6, [2000, 133]),       # tcgen05 kernel, NP=32, runtime R=24
+    ("tc_generic_26",  2, 16, 8, 128, 13, [2000, 133]),      # tcgen05 kernel, NP=32, runtime R=26
+    # compile-time row counts of the paper's operating points (Llama-3.1 gamma 5/6/7/8/11, Qwen2.5 gamma 5)
+    ("tc_ct_24",       2, 32, 8, 128, 6, [1900, 411]),
+    ("tc_ct_28",       2, 32, 8, 128, 7, [1300, 129]),
+    ("tc_ct_32",       2, 32, 8, 128, 8, [2222, 64]),
+    ("tc_ct_36",       2, 32, 8, 128, 9, [1700, 900]),
+    ("tc_ct_42",       2, 28, 4, 128, 6, [2600, 150]),
+    ("tc_ct_48",       3, 32, 8, 128, 12, [1500, 700, 12]),
     ("tc_generic_40",  2, 16, 2, 128, 5, [1500, 700]),       # tcgen05 kernel, NP=48, runtime R=40
     ("tc_np16_16",     2, 8, 2, 128, 4, [900, 260]),         # tcgen05 kernel, NP=16, R=16
     # R > 48: the tcgen05 kernel's row groups (NG = NP / 32 groups of 32 rows, SURVEY §8(b) g*T <= 128)

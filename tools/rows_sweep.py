@@ -59,5 +59,11 @@ def run(name, B, Hq, Hkv, ctx, gammas, rot=2, reps=10):
 
 if __name__ == "__main__":
     md.load_library()
-    run("qwen_100k", 64, 28, 4, 100000, [4, 5, 6, 7, 10, 15])
-    run("llama3_b64_32k", 64, 32, 8, 32768, [4, 11, 15])
+    which = sys.argv[1] if len(sys.argv) > 1 else "baseline"
+    if which == "baseline":
+        run("qwen_100k", 64, 28, 4, 100000, [4, 5, 6, 7, 10, 15])
+        run("llama3_b64_32k", 64, 32, 8, 32768, [4, 11, 15])
+    elif which == "llama_gammas":  # every gamma of the Llama-3.1 GQA shape (R = 4 (gamma + 1))
+        run("llama3_b64_32k", 64, 32, 8, 32768, list(range(2, 16)))
+    elif which == "paper":  # the paper's Llama-3.1-8B SnapKV rows: prefill 100k, bsz 41, gamma 6/7/8/11
+        run("llama3_b41_100k", 41, 32, 8, 100000, [6, 7, 8, 11])
