@@ -530,7 +530,9 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
         for (int j = 0; j < JR; ++j) row[j] = rows_next[j];
         const int npos = pos + TK;
         if (npos < re) load_rows(npos, min(TK, re - npos), rows_next);
-        if (lane == 0) mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
+        // every copying lane acquires the stage itself (the consumers' release of its previous
+        // contents), so no lane's copies rely on ordering through another lane
+        mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
         __syncwarp();
         const uint32_t kt_a = smem_u32(kt) + g8 * 128, vt_a = smem_u32(vt) + g8 * 128;
 #pragma unroll
@@ -551,9 +553,9 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
             cp_async16_pol(vt_a + dst, vs + c * 8, pol);
           }
         }
-        cp_async_arrive(&full[stage]);  // fires when this lane's copies have landed
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[stage]);
+        // MODE_INDEXED: full[] expects one arrival per producer lane; this one fires when the
+        // lane's copies have landed
+        cp_async_arrive_noinc(&full[stage]);
         continue;
       }
       if (p.unit_dyn && p.kn != nullptr && tile_has_new(p, n, pos, nvalid)) {
@@ -572,7 +574,15 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
         fence_proxy_async_global();
         __syncwarp();
       }
-      if (lane != 0) continue;
+      if (gathered0) {  // MODE_INDEXED (the streamed tail): full[] expects all 32 producer lanes
+        mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
+        if (lane != 0) {
+          mbar_arrive(&full[stage]);
+          continue;
+        }
+      } else if (lane != 0) {
+        continue;
+      }
       if (apb != nullptr && tile_has_new(p, n, pos, nvalid)) mbar_wait(apb, 0);  // fused append done
       mbar_wait(&empty[stage], ((it / NSTAGE) & 1) ^ 1);
       if (nvalid == TK) {  // full tile: one TK-row box per 128-byte column slab
@@ -1111,7 +1121,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], p.mode == MODE_INDEXED ? 32 : 1);  // indexed: every producer lane arrives
       mbar_init(&empty[s], NC);
     }
     for (int s = 0; s < 2; ++s) {

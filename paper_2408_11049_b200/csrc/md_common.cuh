@@ -183,4 +183,9 @@ MD_DEV void cp_async16_pol(uint32_t dst, const void* src, uint64_t policy) {
 MD_DEV void cp_async_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// the same, counted as one of the barrier's expected arrivals (.noinc: the pending count is not
+// raised, so the barrier's init count includes this thread)
+MD_DEV void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 }  // namespace md

@@ -65,6 +65,42 @@ def main():
         cnt = torch.zeros(B, dtype=torch.int32, device="cuda")
         md.snapkv_select(case.k, case.v, q_obs, torch.tensor(L, dtype=torch.int32).cuda(), max(L), w, budget,
                          case.scale, idx, cnt)
+    if which in ("all", "tc_ct"):  # compile-time row counts (round 2): R = 24 / 36 / 42 / 48
+        verify(AttnCase(2, 32, 8, 128, 1400, [1400, 300], T=6, seed=9).to_cuda(), 6)
+        verify(AttnCase(2, 32, 8, 128, 1400, [1400, 300], T=9, seed=10).to_cuda(), 9)
+        verify(AttnCase(2, 28, 4, 128, 1400, [1400, 300], T=6, seed=11).to_cuda(), 6)
+        verify(AttnCase(2, 32, 8, 128, 1400, [1400, 300], T=12, seed=12).to_cuda(), 12, fused=True)
+    if which in ("all", "indexed"):  # listed-row copies (8 rows x 64 B per instruction), plain and fused
+        B, Hq, Hkv, d, K = 3, 32, 8, 128, 200
+        L = [1800, 1100, 300]
+        case = AttnCase(B, Hq, Hkv, d, 1850, L, T=1, seed=13).to_cuda()
+        rng = np.random.default_rng(13)
+        idx = np.zeros((B, Hkv, 200), np.int32)
+        for b in range(B):
+            for u in range(Hkv):
+                idx[b, u, :K] = np.sort(rng.choice(L[b] - 64, size=K, replace=False))
+        idx_t = torch.from_numpy(idx).cuda()
+        cnt = torch.full((B,), K, dtype=torch.int32, device="cuda")
+        tail = torch.tensor([n - 40 for n in L], dtype=torch.int32, device="cuda")
+        out = torch.empty((B, Hq, d), device="cuda")
+        ws = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, 1, 1850), dtype=torch.uint8, device="cuda")
+        md.draft_attn_indexed(case.qd, case.k, case.v, case.kv_len_t, idx_t, cnt, tail, case.scale, out, None, ws)
+        kn = bits_to_torch_bf16(S.k_to_bf16_bits(S.new_kv_k(14, S.T_KNEW, B, 1, Hkv, d)))
+        md.draft_attn_indexed(case.qd, case.k, case.v, case.kv_len_t, idx_t, cnt, tail, case.scale, out, None, ws,
+                              k_new=kn, v_new=kn)
+    if which in ("all", "pq"):  # PQ encode / LUT / score / select
+        B, Hq, Hkv, d = 2, 32, 8, 128
+        L = [3000, 1700]
+        case = AttnCase(B, Hq, Hkv, d, 3000, L, T=1, seed=15).to_cuda()
+        pos = S.pq_codebook_positions(15, B, Hkv, L)
+        cb = bits_to_torch_bf16(S.pq_codebook_bits(case.k_bits, pos))
+        codes = torch.zeros((B, Hkv, 3000, 16), dtype=torch.uint8, device="cuda")
+        md.pq_encode(case.k, case.v, cb, torch.zeros(B, dtype=torch.int32, device="cuda"), 3000, codes)
+        idx = torch.zeros((B, Hkv, 4 + 256), dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(B, dtype=torch.int32, device="cuda")
+        tail = torch.zeros(B, dtype=torch.int32, device="cuda")
+        ws = torch.zeros(md.pq_workspace_bytes(B, Hkv, 3000), dtype=torch.uint8, device="cuda")
+        md.pq_select(case.qd, cb, codes, case.kv_len_t, 3000, 4, 128, 256, idx, cnt, tail, ws)
     torch.cuda.synchronize()
     print("sanitize cases done:", which)
 
