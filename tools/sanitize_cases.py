@@ -101,6 +101,35 @@ def main():
         tail = torch.zeros(B, dtype=torch.int32, device="cuda")
         ws = torch.zeros(md.pq_workspace_bytes(B, Hkv, 3000), dtype=torch.uint8, device="cuda")
         md.pq_select(case.qd, cb, codes, case.kv_len_t, 3000, 4, 128, 256, idx, cnt, tail, ws)
+    if which in ("all", "misc"):  # acceptance (sample / greedy), tree acceptance, compaction, append, philox
+        B, gamma, V, T = 4, 4, 1000, 5
+        rng = np.random.default_rng(16)
+        p = rng.random((B, gamma + 1, V)) ** 4
+        p /= p.sum(-1, keepdims=True)
+        q = rng.random((B, gamma, V)) ** 4
+        q /= q.sum(-1, keepdims=True)
+        pt = torch.from_numpy(p.astype(np.float32)).cuda()
+        qt = torch.from_numpy(q.astype(np.float32)).cuda()
+        dt = torch.from_numpy(rng.integers(0, V, (B, gamma)).astype(np.int32)).cuda()
+        rnd = torch.zeros((B, T + 1), dtype=torch.int32, device="cuda")
+        md.philox_u32(17, 3, rnd)
+        ot = torch.zeros((B, gamma + 1), dtype=torch.int32, device="cuda")
+        na = torch.zeros(B, dtype=torch.int32, device="cuda")
+        md.spec_accept(pt, qt, dt, rnd[:, :gamma + 2].contiguous(), ot, na)
+        md.spec_accept(pt, qt, dt, rnd[:, :gamma + 2].contiguous(), ot, na, mode="greedy")
+        ptr_ = torch.from_numpy((rng.random((B, T, V)) ** 4).astype(np.float32)).cuda()
+        ptr_ /= ptr_.sum(-1, keepdim=True)
+        qtr = torch.from_numpy((rng.random((B, T, V)) ** 4).astype(np.float32)).cuda()
+        qtr /= qtr.sum(-1, keepdim=True)
+        parent = torch.tensor([[-1, 0, 0, 1, 1]] * B, dtype=torch.int32, device="cuda")
+        tok = torch.from_numpy(rng.integers(0, V, (B, T)).astype(np.int32)).cuda()
+        otr = torch.zeros((B, T), dtype=torch.int32, device="cuda")
+        nodes = torch.zeros((B, T), dtype=torch.int32, device="cuda")
+        md.spec_accept_tree(ptr_, qtr, tok, parent, rnd, otr, na, accepted_nodes=nodes)
+        case = AttnCase(B, 8, 2, 128, 300, [290, 200, 100, 50], T=T, seed=18).to_cuda()
+        md.kv_compact(case.k, case.v, torch.tensor([280, 190, 90, 40], dtype=torch.int32, device="cuda"), nodes, na)
+        kn = bits_to_torch_bf16(S.k_to_bf16_bits(S.new_kv_k(19, S.T_KNEW, B, T, 2, 128)))
+        md.kv_append(case.k, case.v, kn, kn, torch.tensor([5, 100, 60, 0], dtype=torch.int32, device="cuda"))
     torch.cuda.synchronize()
     print("sanitize cases done:", which)
 
