@@ -414,9 +414,10 @@ def run_gpu(args):
                                             k_new=kn_, v_new=vn_)
                     xd.barrier()
                     continue
-                if fused:
+                if fused:  # MD_ATTN_EARLY_KV: pos is written by torch.add (an ordinary kernel) before the
+                    # first call and the previous call appends into another layer's cache (header contract)
                     md.draft_attn_sparse_append(qd, kb, vb, knew_d, vnew_d, pos[j + 1], sink, window, scale, out_d,
-                                                lse_d, ws_d)
+                                                lse_d, ws_d, early_kv=True)
                 else:
                     md.draft_attn_sparse(qd, kb, vb, pos[j + 1], sink, window, scale, out_d, lse_d, ws_d)
                 if tp > 1:
@@ -540,7 +541,7 @@ def run_gpu(args):
         v_ms = time_calls(lambda r: md.verify_attn_full_append(qv, kc[r % R], vc[r % R], knew_v, vnew_v, kv_len_v,
                                                                max_kv, scale, out_v, lse_v, ws_v))
         d_ms = time_calls(lambda r: md.draft_attn_sparse_append(qd, kc[r % R], vc[r % R], knew_d, vnew_d, kv_len_d,
-                                                                sink, window, scale, out_d, lse_d, ws_d))
+                                                                sink, window, scale, out_d, lse_d, ws_d, early_kv=True))
     else:
         v_ms = time_calls(lambda r: md.verify_attn_full(qv, kc[r % R], vc[r % R], kv_len_v, max_kv, scale, out_v,
                                                         lse_v, ws_v))
@@ -767,7 +768,7 @@ def e2e_measure(args, md, torch, dist, dev, world, tp, tp_group, gamma, layers, 
                 j = c // layers
                 if fused:
                     md.draft_attn_sparse_append(q_, kb, vb_, k_, v_, pos_buf[j + 1], sink, window, scale, out_d,
-                                                lse_d, ws_d)
+                                                lse_d, ws_d, early_kv=True)
                 else:
                     md.kv_append(kb, vb_, k_, v_, pos_buf[j])
                     md.draft_attn_sparse(q_, kb, vb_, pos_buf[j + 1], sink, window, scale, out_d, lse_d, ws_d)

@@ -252,6 +252,28 @@ MD_API md_status md_draft_attn_sparse_append(const md_kv_cache* cache, const voi
                                       size_t workspace_bytes, md_stream_t stream);
 
 /*
+ * md_draft_attn_sparse_append_ex — md_draft_attn_sparse_append with option flags (0 = identical).
+ *
+ *   MD_ATTN_EARLY_KV: the caller guarantees that kv_len[] and the cache rows this call attends to,
+ *     other than the row it appends itself, are not written by an md_* call that precedes it on
+ *     the stream without an intervening ordinary kernel, copy, event wait or host synchronisation
+ *     (this library's kernels let the next kernel launch early, before they finish; ordinary
+ *     work does not).  The kernel may then read kv_len and stream the first key tiles of a unit
+ *     (never one holding the appended row, never q) before waiting for the previous kernel, so
+ *     the call's ramp overlaps the previous call's tail (a draft step: every layer's call, the
+ *     layers' caches distinct from the previous call's).  Results are bit-identical with and
+ *     without the flag; without the guarantee the flag is a data race.  Used only where the draft
+ *     runs the unit-aligned plan (always at head_dim 128 / 64 with g <= 8); ignored otherwise.
+ * Errors: as md_draft_attn_sparse_append; MD_ERR_INVALID_ARG for an unknown flag bit.
+ */
+#define MD_ATTN_EARLY_KV 1u
+MD_API md_status md_draft_attn_sparse_append_ex(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                         const void* k_new, const void* v_new, const int32_t* kv_len,
+                                         int32_t sink, int32_t window, float scale, float* out, float* lse,
+                                         void* workspace, size_t workspace_bytes, uint32_t flags,
+                                         md_stream_t stream);
+
+/*
  * md_draft_attn_indexed — self-speculative draft attention over a static SnapKV-selected KV
  * (the paper's best drafter; SnapKV with observation
  * window 32 and average pooling 5; per-sequence budgets).

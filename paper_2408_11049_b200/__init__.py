@@ -33,7 +33,7 @@ ABI_SYMBOLS = ("md_abi_version", "md_last_error", "md_kv_append", "md_attn_works
                "md_philox_u32_dev", "md_draft_attn_sparse_windows", "md_verify_attn_full_append",
                "md_draft_attn_sparse_append", "md_verify_attn_full_tp_append", "md_draft_attn_sparse_tp_append",
                "md_draft_attn_indexed_append", "md_attn_workspace_bytes_det", "md_verify_attn_full_det",
-               "md_draft_attn_sparse_det")
+               "md_draft_attn_sparse_det", "md_draft_attn_sparse_append_ex")
 
 
 class MDError(RuntimeError):
@@ -91,6 +91,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                                c_void_p, c_void_p, c_void_p, sz, c_void_p]
     lib.md_draft_attn_sparse_append.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, c_void_p, i32, i32, f32,
                                                 c_void_p, c_void_p, c_void_p, sz, c_void_p]
+    lib.md_draft_attn_sparse_append_ex.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, c_void_p, i32, i32, f32,
+                                                   c_void_p, c_void_p, c_void_p, sz, ctypes.c_uint32, c_void_p]
     lib.md_draft_attn_indexed_append.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, c_void_p, c_void_p, i32,
                                                  c_void_p, c_void_p, f32, c_void_p, c_void_p, c_void_p, sz, c_void_p]
     lib.md_draft_attn_indexed.argtypes = [pc, c_void_p, i32, c_void_p, c_void_p, i32, c_void_p, c_void_p, f32,
@@ -274,14 +276,24 @@ def verify_attn_full_append(q, k_cache, v_cache, k_new, v_new, kv_len, max_kv_le
                                           _ptr(lse), ws, wsb, _stream(stream)))
 
 
+MD_ATTN_EARLY_KV = 1
+
+
 def draft_attn_sparse_append(q, k_cache, v_cache, k_new, v_new, kv_len, sink, window, scale, out, lse=None,
-                             workspace=None, stream=None):
+                             workspace=None, stream=None, early_kv=False):
     """kv_append(k_new, v_new at kv_len - 1) fused into draft_attn_sparse: one kernel launch.
-    k_new / v_new [B, 1, Hkv, d] bf16 contiguous."""
+    k_new / v_new [B, 1, Hkv, d] bf16 contiguous.  early_kv: md_draft_attn_sparse_append_ex with
+    MD_ATTN_EARLY_KV (the caller's guarantee of the header: kv_len and the attended rows are not
+    written by the md_* call just before this one on the stream)."""
     _need_contiguous(k_new, v_new)
     lib = load_library()
     c = make_cache(k_cache, v_cache)
     ws, wsb = _ws(workspace)
+    if early_kv:
+        _check(lib.md_draft_attn_sparse_append_ex(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(k_new), _ptr(v_new),
+                                                  _ptr(kv_len), int(sink), int(window), float(scale), _ptr(out),
+                                                  _ptr(lse), ws, wsb, MD_ATTN_EARLY_KV, _stream(stream)))
+        return
     _check(lib.md_draft_attn_sparse_append(ctypes.byref(c), _ptr(q), q.shape[1], _ptr(k_new), _ptr(v_new),
                                            _ptr(kv_len), int(sink), int(window), float(scale), _ptr(out), _ptr(lse),
                                            ws, wsb, _stream(stream)))

@@ -110,6 +110,9 @@ struct AttnParams {
   // fused append is then done by the producer warp right before it issues a tile holding a new row
   int unit_dyn;
   int cap;                // cache capacity (rows), for the MD_DEBUG precondition checks
+  // MD_ATTN_EARLY_KV (draft, unit-aligned keys kernel): the producer streams the first tiles of its
+  // first unit before the grid-dependency wait (kv_len and those rows are final; see the header)
+  int early_kv;
 };
 
 // ------------------------------------------------------------------ stream-K decomposition
@@ -488,10 +491,15 @@ __device__ __forceinline__ void store_out(const AttnParams& p, int64_t off, V v)
 // Stream the K/V tiles of one segment into the ring; `it` is the running tile counter.
 // Called by all 32 lanes of the producer warp (lane 0 owns the barriers; in MODE_INDEXED
 // every lane copies 2 listed rows of an index-list tile with cp.async).
+// skip / limit / stop_at_new (MD_ATTN_EARLY_KV): the first `skip` tiles of the segment were issued
+// already (their `it` slots are passed over), at most `limit` tiles are issued, and with stop_at_new
+// the walk stops before a tile holding one of the call's new rows.  Returns the tiles issued.
 template <int D, int NSTAGE>
-__device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapSet& tm, const Ranges& rg, int b,
-                                                int kvh, uint8_t* ring, uint64_t* full, uint64_t* empty, int& it,
-                                                uint64_t pol, int n = 0, uint64_t* apb = nullptr) {
+__device__ __forceinline__ int produce_segment(const AttnParams& p, const TmapSet& tm, const Ranges& rg, int b,
+                                               int kvh, uint8_t* ring, uint64_t* full, uint64_t* empty, int& it,
+                                               uint64_t pol, int n = 0, uint64_t* apb = nullptr, int skip = 0,
+                                               int limit = 0x7fffffff, bool stop_at_new = false) {
+  int tix = 0, issued = 0;
   constexpr int SUB = D / 64, TILE = TK * D * 2, STAGE = 2 * TILE;
   const int lane = threadIdx.x & 31;
   const bool gathered0 = (p.mode == MODE_INDEXED);
@@ -519,11 +527,14 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
   for (int part = 0; part < 2; ++part) {
     const int rs = part ? rg.s1 : rg.s0, re = part ? rg.e1 : rg.e0;
 #pragma unroll 1
-    for (int pos = rs; pos < re; pos += TK, ++it) {
+    for (int pos = rs; pos < re; pos += TK, ++it, ++tix) {
       const int stage = it % NSTAGE;
       const int nvalid = min(TK, re - pos);
       uint8_t* kt = ring + stage * STAGE;
       uint8_t* vt = kt + TILE;
+      if (tix < skip) continue;  // issued before the grid-dependency wait
+      if (issued == limit || (stop_at_new && tile_has_new(p, n, pos, nvalid))) return issued;
+      ++issued;
       if (part == 0 && gathered0) {
         int row[JR];
 #pragma unroll
@@ -603,6 +614,7 @@ __device__ __forceinline__ void produce_segment(const AttnParams& p, const TmapS
       }
     }
   }
+  return issued;
 }
 
 // ------------------------------------------------------------------ cross-CTA finish
@@ -1146,6 +1158,24 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     prefetch_tmap(&tm.v_part);
   }
   if (p.pdl_early) pdl_trigger();  // else the dependent launch waits for this grid's exit
+  // MD_ATTN_EARLY_KV: kv_len and the rows of the first tiles are final (header contract), so the
+  // producer issues up to NSTAGE tiles of its first unit -- never one holding a new row, never Q --
+  // before the grid-dependency wait: they stream while the previous kernel's last CTAs finish
+  int pre_issued = 0;
+  if (MD_DIRECT_UNITS && p.unit_aligned && p.early_kv) {
+    __syncthreads();  // the barrier initialisation above is visible to the producer
+    if (warp == NC) {
+      const int U0 = p.B * p.Hkv, G0 = gridDim.x;
+      SegWalker w0;
+      w0.init_units((int)((int64_t)blockIdx.x * U0 / G0), (int)((int64_t)(blockIdx.x + 1) * U0 / G0));
+      Seg s0;
+      if (w0.next(p, pre, s0)) {
+        int it0 = 0;
+        pre_issued = produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, s0), s0.b, s0.kvh, smem, full, empty, it0,
+                                                policy_evict_first(), s0.n, nullptr, 0, NSTAGE, true);
+      }
+    }
+  }
   pdl_wait();  // kv_len, the cache and q may come from the previous kernel
   trace_stamp(p, 1);
   // Unit-aligned plan (draft calls): CTA c owns the whole units [c*U/G, (c+1)*U/G), G = gridDim.x,
@@ -1245,7 +1275,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       }
       __syncwarp();
       produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol, sg.n,
-                                 (p.kn != nullptr && !p.unit_dyn) ? apb : nullptr);
+                                 (p.kn != nullptr && !p.unit_dyn) ? apb : nullptr, qi == 0 ? pre_issued : 0);
       ++qi;
     }
     if (lane == 0) trace_put(p, 10, globaltimer());
@@ -1707,6 +1737,7 @@ struct IndexedArgs {
   const void* k_new = nullptr;          // fused append (md_*_append): [B][T][Hkv][d] rows for [n-T, n)
   const void* v_new = nullptr;
   int max_keys = 0;                     // fused append / det: upper bound of the keys per unit (plan choice)
+  bool early_kv = false;                // MD_ATTN_EARLY_KV
   int det_split_tiles = 0;              // deterministic fixed-split plan (md_*_det): piece length in tiles
 };
 
@@ -1842,6 +1873,7 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.unit_aligned = unit_aligned ? 1 : 0;
   p.unit_dyn = unit_dyn ? 1 : 0;
   p.cap = c->capacity;
+  p.early_kv = (ix.early_kv && unit_aligned && MD_DIRECT_UNITS && mode == MODE_DRAFT) ? 1 : 0;
   if (unit_aligned || unit_dyn) p.dyn_k = 0;
   if (p.det_split > 0) p.dyn_k = 0;
   const size_t slots = partial_slots(grid, units, R, det_maxp);
@@ -2051,6 +2083,29 @@ extern "C" md_status md_draft_attn_sparse_append(const md_kv_cache* cache, const
   ix.max_keys = (int)std::min<int64_t>((int64_t)sink + window, cache->capacity);
   return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, out, lse, workspace,
                        workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_append", ix);
+}
+
+extern "C" md_status md_draft_attn_sparse_append_ex(const md_kv_cache* cache, const void* q, int32_t num_q_heads,
+                                                    const void* k_new, const void* v_new, const int32_t* kv_len,
+                                                    int32_t sink, int32_t window, float scale, float* out, float* lse,
+                                                    void* workspace, size_t workspace_bytes, uint32_t flags,
+                                                    md_stream_t stream) {
+  using namespace md;
+  clear_error();
+  MD_REQUIRE(cache != nullptr, MD_ERR_INVALID_ARG, "md_draft_attn_sparse_append_ex: NULL cache");
+  MD_REQUIRE(k_new != nullptr && v_new != nullptr, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_append_ex: NULL k_new/v_new");
+  MD_REQUIRE(sink >= 0 && window >= 1, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_append_ex: need sink >= 0 and window >= 1 (the draft token attends to itself)");
+  MD_REQUIRE((flags & ~(uint32_t)MD_ATTN_EARLY_KV) == 0, MD_ERR_INVALID_ARG,
+             "md_draft_attn_sparse_append_ex: unknown flags 0x%x", (unsigned)flags);
+  IndexedArgs ix;
+  ix.k_new = k_new;
+  ix.v_new = v_new;
+  ix.max_keys = (int)std::min<int64_t>((int64_t)sink + window, cache->capacity);
+  ix.early_kv = (flags & MD_ATTN_EARLY_KV) != 0;
+  return run_attention(cache, q, num_q_heads, 1, kv_len, sink, window, MODE_DRAFT, scale, out, lse, workspace,
+                       workspace_bytes, (cudaStream_t)stream, "md_draft_attn_sparse_append_ex", ix);
 }
 
 extern "C" md_status md_verify_attn_full_tp_append(const md_kv_cache* cache, const void* q, int32_t num_q_heads,

@@ -231,3 +231,69 @@ def test_indexed_draft_append_parity(B, Hq, Hkv, d, lens, counts, stride, win):
     ro, rl = SK.draft_attn_indexed(case.qd_bits, kc, vc, case.kv_len, idx, counts, tails, case.scale)
     _cmp(out.cpu().numpy(), lse.cpu().numpy(), ro, rl)
     assert np.array_equal(_bits(case.k), kc) and np.array_equal(_bits(case.v), vc)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,lens,sink,window", [
+    (3, 32, 8, 128, [3000, 1100, 70], 4, 1020),     # long, medium, a unit of 2 tiles (new row in the 2nd)
+    (2, 28, 4, 128, [2500, 40], 4, 2044),           # Qwen2.5 group of 7; a single-tile unit
+    (4, 32, 32, 128, [900, 800, 513, 2], 4, 508),   # MHA (Llama-2); n = 2
+    (2, 4, 4, 64, [256, 255], 4, 60),               # head_dim 64
+])
+def test_draft_append_early_kv_bit_identical(B, Hq, Hkv, d, lens, sink, window):
+    """MD_ATTN_EARLY_KV (md_draft_attn_sparse_append_ex): the producer streams a unit's first tiles
+    before the grid-dependency wait.  A chain of draft steps over 4 layer caches, back to back on
+    one stream as in bench.py (each call's predecessor appends into another cache), with and
+    without the flag: every output and both caches bit-identical, and the last call against the
+    oracle."""
+    R, steps = 4, 3
+    L = np.array(lens, dtype=np.int32)
+    cap = int(L.max()) + steps + 3
+
+    def run(early):
+        cases = [AttnCase(B, Hq, Hkv, d, cap, L + steps, seed=300 + r).to_cuda() for r in range(R)]
+        ws = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, 1, sink + window), dtype=torch.uint8, device="cuda")
+        outs = []
+        for j in range(steps):
+            kn, vn = _new_rows(400 + j, B, 1, Hkv, d)
+            kn_t, vn_t = bits_to_torch_bf16(kn), bits_to_torch_bf16(vn)
+            n_t = torch.from_numpy((L + j + 1).astype(np.int32)).cuda()
+            for r in range(R):
+                out = torch.empty((B, Hq, d), device="cuda")
+                lse = torch.empty((B, Hq), device="cuda")
+                md.draft_attn_sparse_append(cases[r].qd, cases[r].k, cases[r].v, kn_t, vn_t, n_t, sink, window,
+                                            cases[r].scale, out, lse, ws, early_kv=early)
+                outs.append((out, lse))
+        torch.cuda.synchronize()
+        return cases, [(o.cpu().numpy(), l.cpu().numpy()) for o, l in outs]
+
+    ce, oe = run(True)
+    cp, op = run(False)
+    for (a, b), (c, e) in zip(oe, op):
+        assert np.array_equal(a.view(np.uint32), c.view(np.uint32)) and np.array_equal(b.view(np.uint32),
+                                                                                     e.view(np.uint32))
+    for x, y in zip(ce, cp):
+        assert np.array_equal(_bits(x.k), _bits(y.k)) and np.array_equal(_bits(x.v), _bits(y.v))
+    # the last call (step steps-1, cache R-1) against the oracle chain of that cache
+    c = AttnCase(B, Hq, Hkv, d, cap, L + steps, seed=300 + R - 1)
+    kc, vc = c.k_bits.copy(), c.v_bits.copy()
+    for j in range(steps):
+        kn, vn = _new_rows(400 + j, B, 1, Hkv, d)
+        OA.kv_append(kc, vc, kn, vn, (L + j).astype(np.int32))
+    ro, rl = OA.draft_attn_sparse(c.qd_bits, kc, vc, (L + steps).astype(np.int32), sink, window, c.scale)
+    _cmp(oe[-1][0], oe[-1][1], ro, rl)
+    assert np.array_equal(_bits(ce[-1].k), kc) and np.array_equal(_bits(ce[-1].v), vc)
+
+
+def test_draft_append_ex_rejects_unknown_flags():
+    B, Hq, Hkv, d = 2, 8, 2, 128
+    case = AttnCase(B, Hq, Hkv, d, 300, [300, 200], seed=5).to_cuda()
+    kn = bits_to_torch_bf16(_new_rows(1, B, 1, Hkv, d)[0])
+    lib = md.load_library()
+    c = md.make_cache(case.k, case.v)
+    out = torch.empty((B, Hq, d), device="cuda")
+    ws = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, 1, 64), dtype=torch.uint8, device="cuda")
+    import ctypes
+    st = lib.md_draft_attn_sparse_append_ex(ctypes.byref(c), case.qd.data_ptr(), Hq, kn.data_ptr(), kn.data_ptr(),
+                                            case.kv_len_t.data_ptr(), 4, 60, 0.1, out.data_ptr(), None,
+                                            ws.data_ptr(), ws.numel(), 6, None)
+    assert st == md.MD_ERR_INVALID_ARG and b"unknown flags" in lib.md_last_error()

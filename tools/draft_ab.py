@@ -12,6 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2408_11049_b200 as md  # noqa: E402
 import synth as S  # noqa: E402
 import synth.cuda as SC  # noqa: E402
+from bench import graph_time_calls  # noqa: E402
 
 label = sys.argv[1] if len(sys.argv) > 1 else os.environ.get("MD_LIB", "product")
 # AB_CFG: llama3 (default) | qwen | llama2 | llama3_b128
@@ -41,19 +42,10 @@ scale = float(np.float32(1 / np.sqrt(d)))
 res = {"variant": label, "cfg": cfg}
 for name, call in (("plain", lambda i: md.draft_attn_sparse(q, ks[i % R], vs[i % R], kv, 4, window, scale, out, lse, ws)),
                    ("fused", lambda i: md.draft_attn_sparse_append(q, ks[i % R], vs[i % R], kn, kn, kv, 4, window, scale,
-                                                                   out, lse, ws))):
-    for i in range(8):
-        call(i)
-    torch.cuda.synchronize()
-    ts = []
-    for rep in range(5):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for i in range(64):
-            call(i)
-        b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b) / 64 * 1e3)
+                                                                   out, lse, ws)),
+                   ("fused_early", lambda i: md.draft_attn_sparse_append(q, ks[i % R], vs[i % R], kn, kn, kv, 4, window,
+                                                                         scale, out, lse, ws, early_kv=True))):
+    ts = [graph_time_calls(call, 64, R) * 1e3 for _ in range(5)]  # CUDA-graph replays of 64 calls
     res[name + "_us"] = [round(x, 2) for x in ts]
     res[name + "_us_median"] = round(float(np.median(ts)), 2)
 by = B * Hkv * (window + 4) * d * 4

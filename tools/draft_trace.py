@@ -48,6 +48,8 @@ ends_by_sm = {}
 for c in range(6):
     tr = torch.zeros((1024, 16), dtype=torch.int64, device="cuda")
     md.debug_trace(tr)
+    if c % 2 == 1:  # odd calls: traced with a predecessor in flight (its stamps are overwritten)
+        call(c + 1)
     call(c)
     torch.cuda.synchronize()
     md.debug_trace(None)
@@ -60,7 +62,10 @@ for c in range(6):
     for s_, e_ in zip(sm, end):
         ends_by_sm.setdefault(int(s_), []).append(float(e_))
     located = (t[:, 2] - t1) / 1e3
+    entry = (t[:, 0] - t1) / 1e3
     row = {"ctas": int(len(t)), "start_p50": round(float(np.median(start)), 2),
+           "with_predecessor": bool(c % 2 == 1),
+           "entry_before_release_p0_p50_p100": [round(float(np.percentile(entry, x)), 2) for x in (0, 50, 100)],
            "range_located_p50_p100": [round(float(np.percentile(located, x)), 2) for x in (50, 100)],
            "first_tile_p0_p50_p100": [round(float(np.percentile(first, x)), 2) for x in (0, 50, 100)],
            "end_p0_p10_p50_p90_p100": [round(float(np.percentile(end, x)), 2) for x in (0, 10, 50, 90, 100)],
