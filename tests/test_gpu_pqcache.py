@@ -177,3 +177,63 @@ def test_pq_fullsize_sampled_units():
         want = np.concatenate([np.arange(s0), PQ.select_topk(sc, s0, t0, c)])
         assert int(cnt[b]) == s0 + c and int(tail[b]) == t0
         assert np.array_equal(idx[b, u, :s0 + c].cpu().numpy(), want)
+
+
+def test_gpu_pq_against_the_fp64_definition_offgrid():
+    """The GPU path against the plain PQ definition, independently of the oracle's fixed-point
+    arithmetic (16 sub-vectors x 8-bit codes; readings Z25-Z29): on off-grid bf16 keys,
+    queries and codebooks, (1) every GPU code is the fp64 nearest centroid up to the fp32 rounding
+    bound of the squared distance, (2) the GPU selection is the exact top-k of the fp64 PQ scores
+    q . k_hat computed from the GPU's own codes, except positions whose score ties the k-th within
+    twice the derived score bound (the check of test_oracle_pqcache, applied to the GPU)."""
+    U = 2.0 ** -24
+    rng = np.random.default_rng(31)
+    B, Hq, Hkv, d, g = 2, 16, 4, 128, 4
+    s = d // 16
+    lens = [2500, 1800]
+    sink, window, budget = 4, 128, 300
+    case = AttnCase(B, Hq, Hkv, d, max(lens) + 8, lens, seed=31)
+    case.k_bits = _rand_bf16(rng, case.k_bits.shape, 1.0)
+    case.to_cuda()
+    cb = _rand_bf16(rng, (B, Hkv, 16, 256, s), 1.0)
+    q_bits = _rand_bf16(rng, case.qd_bits.shape, 1.0)
+    codes = _encode_gpu(case, cb, np.zeros(B), max(lens), max(lens) + 8)
+    idx, cnt, tail = _select_gpu(case, q_bits, cb, codes, sink, window, budget, max(lens))
+    codes = codes.cpu().numpy()
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    f64 = lambda bits: S.bf16_bits_to_f32(bits).astype(np.float64)
+    ncode_diff = nsel_diff = 0
+    for b in range(B):
+        nb = lens[b]
+        s0, t0 = min(sink, nb), max(min(sink, nb), nb - window)
+        c = min(budget, t0 - s0)
+        assert int(cnt[b]) == s0 + c and idx[b, 0, :s0].tolist() == list(range(s0))
+        for u in range(Hkv):
+            X, C = f64(case.k_bits[b, u, :nb]), f64(cb[b, u])
+            for m in range(16):
+                diff = X[:, None, m * s:(m + 1) * s] - C[m][None]
+                dist = (diff ** 2).sum(-1)
+                best = np.argmin(dist, axis=1)
+                bound = (s + 2) * U * dist
+                gc = codes[b, u, :nb, m].astype(np.int64)
+                bad = np.nonzero(gc != best)[0]
+                ncode_diff += len(bad)
+                for j in bad:
+                    assert dist[j, gc[j]] - dist[j, best[j]] <= bound[j, gc[j]] + bound[j, best[j]], (b, u, m, j)
+            Q = f64(q_bits[b, u * g:(u + 1) * g])
+            khat = np.concatenate([C[m][codes[b, u, :nb, m]] for m in range(16)], axis=1)
+            exact = khat @ Q.sum(0)
+            absterm = np.stack([np.abs(C[m]) @ np.abs(Q[:, m * s:(m + 1) * s]).sum(0) for m in range(16)])
+            lut_max = max(float(np.max(np.abs(C[m] @ Q[:, m * s:(m + 1) * s].sum(0)))) for m in range(16))
+            e = 26 - int(np.frexp(lut_max)[1])
+            ent = 2 * g * s * U * absterm + 2.0 ** -e  # rint to the 2^-e grid, e within 1 of the fp64 max's
+            sbound = sum(ent[m][codes[b, u, :nb, m]] for m in range(16))
+            cand = np.arange(s0, t0)
+            ref = set(sorted(cand.tolist(), key=lambda j: (-exact[j], j))[:c])
+            got = set(idx[b, u, s0:s0 + c].tolist())
+            thr = np.sort(exact[s0:t0])[::-1][c - 1]
+            for x in ref ^ got:
+                nsel_diff += 1
+                assert abs(exact[x] - thr) <= 2 * sbound.max(), (b, u, x)
+    assert ncode_diff <= B * Hkv * 16 * max(lens) * 1e-3
+    assert nsel_diff <= 8
