@@ -117,6 +117,11 @@ struct AttnParams {
   // MD_ATTN_EARLY_KV (draft, unit-aligned keys kernel): the producer streams the first tiles of its
   // first unit before the grid-dependency wait (kv_len and those rows are final; see the header)
   int early_kv;
+  // unit packing (unit-aligned keys kernel, R <= 4): up to `pack` consecutive units of a CTA share
+  // one pass -- their query rows side by side in the 8 MMA rows (unit s on rows [sR, sR + R)), their
+  // key ranges streamed one after the other, each tile masking the rows of the other units -- so the
+  // CTA runs one epilogue for the group instead of one per unit (1 = off)
+  int pack;
 };
 
 // ------------------------------------------------------------------ stream-K decomposition
@@ -1089,6 +1094,9 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
 #ifndef MD_DIRECT_UNITS
 #define MD_DIRECT_UNITS 1  // unit-aligned keys-kernel calls walk their units without a prefix table (0: A/B builds)
 #endif
+#ifndef MD_PACK_UNITS
+#define MD_PACK_UNITS 1  // unit packing for R <= 4 drafts (AttnParams::pack; 0: A/B builds)
+#endif
 #ifndef MD_EXP_FMA
 #define MD_EXP_FMA 0  // experiment (A/B builds only): R <= 4 draft segments on CUDA-core FMA (fma_segment)
 #endif
@@ -1363,7 +1371,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   // query rows >= R of both Q slots stay zero for the whole kernel
   for (int i = threadIdx.x; i < 2 * C::ROWS * (D / 8); i += C::THREADS) {
     const int row = i / (D / 8), c = i - row * (D / 8);
-    if ((row % C::ROWS) >= p.R) *reinterpret_cast<uint4*>(qbuf + row * C::QSTR + c * 16) = make_uint4(0, 0, 0, 0);
+    if ((row % C::ROWS) >= p.R * p.pack) *reinterpret_cast<uint4*>(qbuf + row * C::QSTR + c * 16) = make_uint4(0, 0, 0, 0);
   }
   trace_stamp(p, 0);
   if (warp == NC && lane == 0) {  // descriptor fetches overlap the grid-dependency wait
@@ -1480,17 +1488,29 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       return true;
     };
     while (next_seg()) {
-      // this segment's query rows: row r = (t = r / g, head = kvh*g + r % g)
+      // this group's query rows: row s*R + r of unit gu0 + s = (t = r / g, head = kvh*g + r % g);
+      // a group is one unit unless the call packs units (p.pack > 1: consecutive whole units, each
+      // with >= 1 key by the header's preconditions)
+      const int gu0 = sg.unit;
+      const int ng = p.pack > 1 ? (int)min((int64_t)p.pack, 1 + walk.end - walk.t) : 1;
       if (lane == 0) {
         const int qs = qi & 1;
         mbar_wait(&qempty[qs], ((qi >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&qfull[qs], p.R * D * 2);
-        for (int r = 0; r < p.R; ++r)
-          bulk_load(qbuf + (qs * C::ROWS + r) * C::QSTR, p.q + out_row(p, sg.b, sg.kvh, r) * D, D * 2, &qfull[qs]);
+        mbar_arrive_expect_tx(&qfull[qs], ng * p.R * D * 2);
+        for (int su = 0; su < ng; ++su) {
+          const int bb = (gu0 + su) / p.Hkv, hh = gu0 + su - bb * p.Hkv;
+          for (int r = 0; r < p.R; ++r)
+            bulk_load(qbuf + (qs * C::ROWS + su * p.R + r) * C::QSTR, p.q + out_row(p, bb, hh, r) * D, D * 2,
+                      &qfull[qs]);
+        }
       }
       __syncwarp();
-      produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol, sg.n,
-                                 (p.kn != nullptr && !p.unit_dyn) ? apb : nullptr, qi == 0 ? pre_issued : 0);
+      for (int su = 0; su < ng; ++su) {
+        if (su > 0) walk.next(p, pre, sg);
+        produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, sg), sg.b, sg.kvh, smem, full, empty, it, pol, sg.n,
+                                   (p.kn != nullptr && !p.unit_dyn) ? apb : nullptr,
+                                   (qi == 0 && su == 0) ? pre_issued : 0);
+      }
       ++qi;
     }
     if (lane == 0) trace_put(p, 10, globaltimer());
@@ -1529,14 +1549,9 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       continue;
     }
 #endif
-    const int n = sg.n;
-    const Ranges rg = seg_ranges(p, sg);
-    // new-key visibility of the two rows 2cq, 2cq+1 this thread holds (verify; rows past R
-    // take the mask of row R-1, their output is dropped)
-    const int vbase = (p.mode == MODE_VERIFY) ? n - p.T : 0x7fffffff;
-    uint32_t msk[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) msk[j] = node_mask(p, sg.b, 2 * cq + j);
+    // a group of ng consecutive whole units (unit packing, p.pack > 1; mirrors the producer) or one segment
+    const int gu0 = sg.unit;
+    const int ng = p.pack > 1 ? (int)min((int64_t)p.pack, 1 + walk.end - walk.t) : 1;
     // Q^T fragments (B operand): qb[kk][0..1] = Q[gq][kk*16 + 2cq (+8) ..]
     uint32_t qb[MD16][2];
     {
@@ -1554,6 +1569,23 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
 #pragma unroll
     for (int i = 0; i < MD16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
     float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+
+#pragma unroll 1
+    for (int su = 0; su < ng; ++su) {
+    if (su > 0) walk.next(p, pre, sg);
+    const int n = sg.n;
+    const Ranges rg = seg_ranges(p, sg);
+    // new-key visibility of the two rows 2cq, 2cq+1 this thread holds (verify; rows past R
+    // take the mask of row R-1, their output is dropped)
+    const int vbase = (p.mode == MODE_VERIFY) ? n - p.T : 0x7fffffff;
+    uint32_t msk[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) msk[j] = node_mask(p, sg.b, 2 * cq + j);
+    // packed group: rows 2cq, 2cq+1 take part in this unit's tiles only if they are its rows
+    bool act[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) act[j] = p.pack == 1 || (2 * cq + j) / p.R == su;
+    const bool packed = p.pack > 1;
 
 #pragma unroll 1
     for (int part = 0; part < 2; ++part) {
@@ -1584,7 +1616,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
             }
           }
           // ---------------- scale, mask, online softmax (log2 domain); rows 2cq, 2cq+1
-          const bool need_mask = (kw0 + KW > nvalid) || (pos + kw0 + KW - 1 >= vbase);
+          const bool need_mask = packed || (kw0 + KW > nvalid) || (pos + kw0 + KW - 1 >= vbase);
           float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
           for (int kb = 0; kb < KB; ++kb)
@@ -1593,7 +1625,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
               float v = s[kb][e] * p.scale_log2;
               if (need_mask) {
                 const int ko = kw0 + kb * 16 + gq + ((e >> 1) << 3);
-                v = (ko >= nvalid || key_hidden(msk[e & 1], pos + ko - vbase)) ? -INFINITY : v;
+                v = (!act[e & 1] || ko >= nvalid || key_hidden(msk[e & 1], pos + ko - vbase)) ? -INFINITY : v;
               }
               s[kb][e] = v;
               mx[e & 1] = fmaxf(mx[e & 1], v);
@@ -1606,7 +1638,8 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
             mx[j] = fmaxf(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], 16));
             const float mn = fmaxf(m[j], mx[j]);
             const float base = (mn == -INFINITY) ? 0.f : mn;
-            corr[j] = ex2(m[j] - base);
+            // (an unchanged maximum, also -inf: the row has seen no key yet, gives exactly 1)
+            corr[j] = (mn == m[j]) ? 1.f : ex2(m[j] - base);
             m[j] = mn;
             float rsum = 0.f;
 #pragma unroll
@@ -1656,6 +1689,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         if (lane == 0) mbar_arrive(&empty[stage]);
       }
     }
+    }  // sub-units of the group
 
     // ============================== segment epilogue ==============================
     trace_stamp(p, 4);
@@ -1735,15 +1769,18 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     const int slot_base = seg_slot(p, pl, sg, chunk);
     {
       constexpr int V4 = D / 4;
-      for (int idx = threadIdx.x; idx < p.R * V4; idx += NC * 32) {
+      for (int idx = threadIdx.x; idx < ng * p.R * V4; idx += NC * 32) {
         const int r = idx / V4, c4 = (idx - r * V4) * 4;
         const int sc = c4 ^ (((r >> 1) & 3) << 3);
         const float4 a = *reinterpret_cast<const float4*>(obuf + r * D + sc);
         const float4 c = *reinterpret_cast<const float4*>(obuf + FRAG + r * D + sc);
         const float4 v = make_float4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
         if (complete) {
-          store_out(p, o_row(p, sg.b, sg.kvh, r) * D + c4, v);
-          if (c4 == 0 && p.lse != nullptr) p.lse[out_row(p, sg.b, sg.kvh, r)] = lsebuf[r] * LN2;
+          // row r of the group = row r % R of unit gu0 + r / R (one unit: gu0 = sg.unit)
+          const int su = r / p.R, rr = r - su * p.R;
+          const int bb = (gu0 + su) / p.Hkv, hh = gu0 + su - bb * p.Hkv;
+          store_out(p, o_row(p, bb, hh, rr) * D + c4, v);
+          if (c4 == 0 && p.lse != nullptr) p.lse[out_row(p, bb, hh, rr)] = lsebuf[r] * LN2;
         } else {
           const int64_t prow = (int64_t)slot_base * p.R + r;
           __stcg(reinterpret_cast<float4*>(p.ws_o + prow * D + c4), v);
@@ -2095,6 +2132,9 @@ static md_status run_attention(const md_kv_cache* c, const void* q, int Hq, int 
   p.unit_dyn = unit_dyn ? 1 : 0;
   p.cap = c->capacity;
   p.early_kv = (ix.early_kv && unit_aligned && MD_DIRECT_UNITS && mode == MODE_DRAFT) ? 1 : 0;
+  p.pack = (MD_PACK_UNITS && !MD_EXP_FMA && unit_aligned && MD_DIRECT_UNITS && use_keys_kernel(R) && R <= 4)
+               ? 8 / R
+               : 1;
   if (unit_aligned || unit_dyn) p.dyn_k = 0;
   if (p.det_split > 0) p.dyn_k = 0;
   const size_t slots = partial_slots(grid, units, R, det_maxp);
