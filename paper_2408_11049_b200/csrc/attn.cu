@@ -1094,6 +1094,12 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
 #ifndef MD_DIRECT_UNITS
 #define MD_DIRECT_UNITS 1  // unit-aligned keys-kernel calls walk their units without a prefix table (0: A/B builds)
 #endif
+#ifndef MD_EARLY_PF
+// early-KV draft prologue: full tiles prefetched into L2 beyond the NSTAGE issued to shared memory
+// (graph-timed sweep 0 / 2 / 3 / 4 / 5 / 6 / 8 / 16 / 32, profiles/draft_ab_r02_early_l2pf*.txt:
+// 3 best, Llama-3.1 47.2 -> 45.8 us, Qwen2.5 45.4 -> 43.7, B = 128 88.6 -> 87.4; 16+ slower)
+#define MD_EARLY_PF 3
+#endif
 #ifndef MD_PACK_UNITS
 #define MD_PACK_UNITS 1  // unit packing for R <= 4 drafts (AttnParams::pack; 0: A/B builds)
 #endif
@@ -1396,6 +1402,31 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         int it0 = 0;
         pre_issued = produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, s0), s0.b, s0.kvh, smem, full, empty, it0,
                                                 policy_evict_first(), s0.n, nullptr, 0, NSTAGE, true);
+        // the next MD_EARLY_PF full tiles of the CTA's units into L2 (a hint: safe whatever the
+        // previous kernel still writes -- L2 is the point of coherence), so the CTAs that become
+        // resident during the previous call's tail fill its idle HBM bandwidth with this call's reads
+        if (MD_EARLY_PF > 0 && lane == 0 && p.mode == MODE_DRAFT) {
+          int left = MD_EARLY_PF, skip = pre_issued;
+          Seg su = s0;
+          do {
+            const Ranges rg = seg_ranges(p, su);
+            for (int part = 0; part < 2 && left > 0; ++part) {
+              const int rs = part ? rg.s1 : rg.s0, re = part ? rg.e1 : rg.e0;
+              for (int pos = rs; pos + TK <= re && left > 0; pos += TK) {
+                if (skip > 0) {
+                  --skip;
+                  continue;
+                }
+                for (int sub = 0; sub < D / 64; ++sub) {
+                  tma_prefetch_4d(&tm.k_full, sub * 64, pos, su.kvh, su.b);
+                  tma_prefetch_4d(&tm.v_full, sub * 64, pos, su.kvh, su.b);
+                }
+                --left;
+              }
+            }
+            skip = 0;
+          } while (left > 0 && w0.next(p, pre, su));
+        }
       }
     }
   }

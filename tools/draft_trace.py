@@ -34,6 +34,10 @@ out = torch.empty((B, Hq, d), device="cuda")
 ws = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, d, 1, 1024), dtype=torch.uint8, device="cuda")
 scale = float(np.float32(1 / np.sqrt(d)))
 call = lambda i: md.draft_attn_sparse(q, ks[i % R], vs[i % R], kv, 4, 1020, scale, out, None, ws)
+if os.environ.get("TRACE_FORM") == "fused_early":  # the form bench.py times: fused append + early KV
+    kn = torch.zeros((B, 1, Hkv, d), dtype=torch.bfloat16, device="cuda")
+    call = lambda i: md.draft_attn_sparse_append(q, ks[i % R], vs[i % R], kn, kn, kv, 4, 1020, scale, out, None, ws,
+                                                 early_kv=True)
 for i in range(8):
     call(i)
 torch.cuda.synchronize()
@@ -43,7 +47,7 @@ for i in range(40):
     call(i)
 b.record()
 torch.cuda.synchronize()
-res = {"call_us_rotated": round(a.elapsed_time(b) / 40 * 1e3, 2), "calls": []}
+res = {"form": os.environ.get("TRACE_FORM", "plain"), "call_us_rotated": round(a.elapsed_time(b) / 40 * 1e3, 2), "calls": []}
 ends_by_sm = {}
 for c in range(6):
     tr = torch.zeros((1024, 16), dtype=torch.int64, device="cuda")
