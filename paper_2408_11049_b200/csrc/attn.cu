@@ -258,13 +258,18 @@ struct SegWalker {
   int64_t t, end, ustart;
   int b, h, tiles_b;
   int umode;  // 1: whole units t .. end-1 by unit index (unit-aligned plan; no prefix table)
-  __device__ void init_units(int u0, int u1) {
+  const int* kvs;  // umode: kv_len of sequences kvs_b0.. staged in shared memory (early-KV calls), or null
+  int kvs_b0;
+  __device__ void init_units(int u0, int u1, const int* stash = nullptr, int stash_b0 = 0) {
     umode = 1;
     t = u0;
     end = u1;
+    kvs = stash;
+    kvs_b0 = stash_b0;
   }
   __device__ void init(const AttnParams& p, const int* pre, int64_t S, int64_t E) {
     umode = 0;
+    kvs = nullptr;
     t = S;
     end = E;
     int64_t acc = 0;
@@ -299,7 +304,7 @@ struct SegWalker {
         sg.b = u / p.Hkv;
         sg.kvh = u - sg.b * p.Hkv;
         sg.unit = u;
-        sg.n = __ldg(p.kv_len + sg.b);
+        sg.n = kvs != nullptr ? kvs[sg.b - kvs_b0] : __ldg(p.kv_len + sg.b);
         check_len(p, sg.b, sg.n);
         sg.tiles = (unit_keys(p, sg.n, sg.b) + TK - 1) / TK;
         sg.lo = 0;
@@ -461,7 +466,8 @@ constexpr int TRACE_SLOTS = 16;
 // Diagnostics (md_debug_trace): slot 0 entry, 1 after the grid-dependency wait, 2 range
 // located, 3 first tile landed, 4 last epilogue start, 5 end, 6 smid, 7 last epilogue after
 // the cross-warp combine, 8 after its stores, 9 after finish_unit, 10 producer done,
-// 11 segments processed.
+// 11 segments processed, 12 consumer warp 0 done with the fused append, 13 first Q landed
+// (consumer warp 0), 14 first Q loads issued (producer).
 __device__ __forceinline__ void trace_put(const AttnParams& p, int k, unsigned long long v) {
   if (p.trace != nullptr) p.trace[blockIdx.x * TRACE_SLOTS + k] = v;
 }
@@ -1331,7 +1337,7 @@ __device__ void fma_segment(const AttnParams& p, const Plan& pl, const Seg& sg, 
 }
 #endif
 
-template <int D, int KS, int CTAS>
+template <int D, int KS, int CTAS, bool EARLY>
 __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     attn_keys_kernel(const __grid_constant__ TmapSet tm, const AttnParams p) {
   using C = KeysCfg<D, KS, CTAS>;
@@ -1391,14 +1397,34 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   // producer issues up to NSTAGE tiles of its first unit -- never one holding a new row, never Q --
   // before the grid-dependency wait: they stream while the previous kernel's last CTAs finish
   int pre_issued = 0;
-  if (MD_DIRECT_UNITS && p.unit_aligned && p.early_kv) {
-    __syncthreads();  // the barrier initialisation above is visible to the producer
+  // early-KV calls also stage the kv_len of the CTA's sequences in shared memory (the prefix-table
+  // space, unused by the unit-aligned walk) before the wait: the walkers then need no global load
+  // after the release (griddepcontrol.wait makes the L1 reload it: ~2 us under a saturated fabric),
+  // and the producer issues the first group's Q loads as its first action after the release
+  const bool stashed = EARLY && MD_DIRECT_UNITS && p.unit_aligned && p.early_kv;
+  const int stash_b0 = (int)((int64_t)blockIdx.x * (p.B * p.Hkv) / gridDim.x) / p.Hkv;
+  int q0_unit = -1, q0_ng = 0;  // producer lane 0: the first group, whose Q loads go out right after the wait
+  if (stashed) {
+    if (warp == NC) {
+      const int U0 = p.B * p.Hkv, G0 = gridDim.x;
+      const int u0 = (int)((int64_t)blockIdx.x * U0 / G0), u1 = (int)((int64_t)(blockIdx.x + 1) * U0 / G0);
+      const int nb = u1 > u0 ? (u1 - 1) / p.Hkv - stash_b0 + 1 : 0;
+      for (int i = lane; i < nb; i += 32) pre[i] = __ldg(p.kv_len + stash_b0 + i);
+    }
+    if (threadIdx.x == 0) {  // the unit-aligned direct plan
+      Plan d{};
+      d.G = d.nch = gridDim.x;
+      *plan_smem = d;
+    }
+    __syncthreads();  // the barrier initialisation, the plan and the stash are visible to every warp
     if (warp == NC) {
       const int U0 = p.B * p.Hkv, G0 = gridDim.x;
       SegWalker w0;
-      w0.init_units((int)((int64_t)blockIdx.x * U0 / G0), (int)((int64_t)(blockIdx.x + 1) * U0 / G0));
+      w0.init_units((int)((int64_t)blockIdx.x * U0 / G0), (int)((int64_t)(blockIdx.x + 1) * U0 / G0), pre, stash_b0);
       Seg s0;
       if (w0.next(p, pre, s0)) {
+        q0_unit = s0.unit;
+        q0_ng = p.pack > 1 ? (int)min((int64_t)p.pack, 1 + w0.end - w0.t) : 1;
         int it0 = 0;
         pre_issued = produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, s0), s0.b, s0.kvh, smem, full, empty, it0,
                                                 policy_evict_first(), s0.n, nullptr, 0, NSTAGE, true);
@@ -1432,13 +1458,22 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   }
   pdl_wait();  // kv_len, the cache and q may come from the previous kernel
   trace_stamp(p, 1);
+  if (stashed && warp == NC && lane == 0 && q0_ng > 0) {  // the first group's Q rows into slot 0
+    mbar_arrive_expect_tx(&qfull[0], q0_ng * p.R * D * 2);
+    for (int su = 0; su < q0_ng; ++su) {
+      const int bb = (q0_unit + su) / p.Hkv, hh = q0_unit + su - bb * p.Hkv;
+      for (int r = 0; r < p.R; ++r)
+        bulk_load(qbuf + (su * p.R + r) * C::QSTR, p.q + out_row(p, bb, hh, r) * D, D * 2, &qfull[0]);
+    }
+    if (p.trace != nullptr) trace_put(p, 14, globaltimer());
+  }
   // Unit-aligned plan (draft calls): CTA c owns the whole units [c*U/G, (c+1)*U/G), G = gridDim.x,
   // so it needs neither the per-sequence prefix table nor a plan -- its producer issues the
   // first tile right after reading its first unit's kv_len (MD_DIRECT_UNITS; the prefix walk
   // costs a batch-wide kv_len load, a scan and two CTA barriers before the first TMA issue)
   const bool direct = MD_DIRECT_UNITS && p.unit_aligned;
   if (direct) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !stashed) {  // (early-KV calls wrote it before the prologue's barrier)
       Plan d{};
       d.G = d.nch = gridDim.x;
       *plan_smem = d;
@@ -1449,14 +1484,18 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     // the plan lives in shared memory (read only at segment boundaries: keeps registers free)
     if (threadIdx.x == 0) *plan_smem = make_plan(p, total_tiles(p, pre), gridDim.x);
   }
-  __syncthreads();
+  // early-KV calls need no CTA barrier after the release: the barriers, the plan and the kv_len
+  // stash were published by the prologue's __syncthreads, so every warp starts its first
+  // post-release loads (producer: Q; consumers: the fused append's new rows) at once
+  if (!stashed) __syncthreads();
   const Plan& pl = *plan_smem;
   if ((int)blockIdx.x >= pl.G) return;  // uniform across the CTA
   int chunk = blockIdx.x;                // this CTA's static chunk, then claimed dynamic ones
   const int U = p.B * p.Hkv;
   auto init_walk = [&](SegWalker& w) {
     if (direct) {
-      w.init_units((int)((int64_t)chunk * U / pl.G), (int)((int64_t)(chunk + 1) * U / pl.G));
+      w.init_units((int)((int64_t)chunk * U / pl.G), (int)((int64_t)(chunk + 1) * U / pl.G), stashed ? pre : nullptr,
+                   stash_b0);
     } else {
       int64_t S0, E0;
       cta_range(p, pre, pl, chunk, S0, E0);
@@ -1473,6 +1512,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     append_own_rows<D>(p, pre, aw, threadIdx.x, NC * 32);
     __syncwarp();
     if (lane == 0) mbar_arrive(apb);
+    trace_stamp(p, 12);
   }
 
   if (warp == NC) {
@@ -1524,7 +1564,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
       // with >= 1 key by the header's preconditions)
       const int gu0 = sg.unit;
       const int ng = p.pack > 1 ? (int)min((int64_t)p.pack, 1 + walk.end - walk.t) : 1;
-      if (lane == 0) {
+      if (lane == 0 && !(qi == 0 && q0_ng > 0)) {  // (the first group's Q went out right after the wait)
         const int qs = qi & 1;
         mbar_wait(&qempty[qs], ((qi >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&qfull[qs], ng * p.R * D * 2);
@@ -1534,6 +1574,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
             bulk_load(qbuf + (qs * C::ROWS + su * p.R + r) * C::QSTR, p.q + out_row(p, bb, hh, r) * D, D * 2,
                       &qfull[qs]);
         }
+        if (qi == 0 && p.trace != nullptr) trace_put(p, 14, globaltimer());
       }
       __syncwarp();
       for (int su = 0; su < ng; ++su) {
@@ -1588,6 +1629,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     {
       const int qs = qi & 1;
       mbar_wait(&qfull[qs], (qi >> 1) & 1);
+      if (qi == 0) trace_stamp(p, 13);
       const uint32_t qrow = qring + (qs * C::ROWS + (lane & 7)) * C::QSTR + (lane >> 3) * 16;
 #pragma unroll
       for (int kk = 0; kk < MD16; kk += 2) ldsm_x4(qrow + kk * 32, qb[kk][0], qb[kk][1], qb[kk + 1][0], qb[kk + 1][1]);
@@ -1951,10 +1993,13 @@ static md_status launch_rows(const TmapSet& tm, const AttnParams& p, int grid, c
 
 template <int D, int KS, int CTAS>
 static md_status launch_keys(const TmapSet& tm, const AttnParams& p, int grid, cudaStream_t s) {
+  // early-KV calls run their own instantiation: the prologue that streams before the grid-dependency
+  // wait is compiled out of every other call (its mere presence cost the plain draft ~0.5 us:
+  // register allocation and scheduling of the whole kernel change with it)
   using C = KeysCfg<D, KS, CTAS>;
-  auto kern = attn_keys_kernel<D, KS, CTAS>;
-  static int done = -1;
-  md_status st = set_smem(kern, C::SMEM, &done);
+  auto kern = p.early_kv ? attn_keys_kernel<D, KS, CTAS, true> : attn_keys_kernel<D, KS, CTAS, false>;
+  static int done[2] = {-1, -1};
+  md_status st = set_smem(kern, C::SMEM, &done[p.early_kv ? 1 : 0]);
   if (st != MD_OK) return st;
   if (launch_pdl(kern, grid, C::THREADS, C::SMEM, s, tm, p) != cudaSuccess) return check_launch("attn_keys_kernel");
   return check_launch("attn_keys_kernel");

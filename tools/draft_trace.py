@@ -79,7 +79,11 @@ for c in range(6):
            "epilogue_phases_p50": {"combine": round(float(np.median(t[:, 7] - t[:, 4])) / 1e3, 2),
                                    "stores": round(float(np.median(t[:, 8] - t[:, 7])) / 1e3, 2),
                                    "to_end": round(float(np.median(t[:, 5] - t[:, 8])) / 1e3, 2)},
-           "producer_done_to_end_p50": round(float(np.median(t[:, 5] - t[:, 10])) / 1e3, 2)}
+           "producer_done_to_end_p50": round(float(np.median(t[:, 5] - t[:, 10])) / 1e3, 2),
+           # after the release: first Q loads issued (producer), fused append done / first Q landed (consumer warp 0)
+           "q_issued_p50_p90": [round(float(np.percentile((t[:, 14] - t1) / 1e3, x)), 2) for x in (50, 90)] if (t[:, 14] > 0).any() else None,
+           "append_done_p50_p90": [round(float(np.percentile((t[:, 12] - t1) / 1e3, x)), 2) for x in (50, 90)] if (t[:, 12] > 0).any() else None,
+           "q_landed_p50_p90": [round(float(np.percentile((t[:, 13] - t1) / 1e3, x)), 2) for x in (50, 90)] if (t[:, 13] > 0).any() else None}
     res["calls"].append(row)
 # per-SM persistence: correlation of an SM's mean end time between even and odd calls
 sms = sorted(ends_by_sm)
