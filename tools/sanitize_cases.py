@@ -101,6 +101,18 @@ def main():
         tail = torch.zeros(B, dtype=torch.int32, device="cuda")
         ws = torch.zeros(md.pq_workspace_bytes(B, Hkv, 3000), dtype=torch.uint8, device="cuda")
         md.pq_select(case.qd, cb, codes, case.kv_len_t, 3000, 4, 128, 256, idx, cnt, tail, ws)
+    if which in ("all", "packed"):  # unit packing (R = 4: pack 2, R = 1: pack 8), fused append, early KV + stash
+        for (B, Hq, Hkv, L0) in ((40, 32, 8, 200), (80, 32, 32, 90)):
+            lens = [L0 - (b % 7) for b in range(B)]
+            c = AttnCase(B, Hq, Hkv, 128, L0, lens, T=1, seed=18).to_cuda()
+            draft(c, 4, 60)
+            draft(c, 4, 60, fused=True)
+            out = torch.empty((B, Hq, 128), device="cuda")
+            ws = torch.zeros(md.attn_workspace_bytes(B, Hq, Hkv, 128, 1, 64), dtype=torch.uint8, device="cuda")
+            kn = bits_to_torch_bf16(S.k_to_bf16_bits(S.new_kv_k(19, S.T_KNEW, B, 1, Hkv, 128)))
+            for _ in range(2):  # back to back: the second call's prologue overlaps the first call's tail
+                md.draft_attn_sparse_append(c.qd, c.k, c.v, kn, kn, c.kv_len_t, 4, 60, c.scale, out, None, ws,
+                                            early_kv=True)
     if which in ("all", "misc"):  # acceptance (sample / greedy), tree acceptance, compaction, append, philox
         B, gamma, V, T = 4, 4, 1000, 5
         rng = np.random.default_rng(16)
