@@ -41,13 +41,13 @@ constexpr int NS = 5;            // cp.async pipeline depth of the score kernel 
 constexpr int SCORE_SMEM = NC * 64 * 4 + 1024 * 4 + NS * SCORE_THREADS * 16;  // table + histogram + ring
 constexpr int HIST1 = 1024;      // pass-1 digit: key bits 31..22
 constexpr int HIST2 = 2048;      // passes 2, 3: bits 21..11, 10..0
-constexpr int TIE_CAP = 2048;    // keys of the cutoff bin kept in shared memory
-// (measured: 256 threads at 4 CTAs/SM -- one wave of the 512 units -- gave 141 -> 136 us of
-// T_select at the Llama-3.1 point but 182 -> 220 us for Qwen2.5's 256 units of 100k candidates)
-constexpr int SEL_THREADS = 512;
 constexpr int RL = 36;           // candidates per select thread run (16-byte loads, no bank conflicts)
-constexpr int SB = SEL_THREADS * RL;  // candidates staged in shared memory per super-block
-constexpr int SEL_SMEM = SB * 4 + TIE_CAP * 6;
+// candidates staged in shared memory per super-block: NT * RL; dynamic shared memory per CTA:
+constexpr int sel_smem(int nt, int tc) { return nt * RL * 4 + tc * 6; }
+// More units than one wave of 512-thread CTAs (2 per SM): 256-thread CTAs, 4 per SM, with a
+// 1024-key tie list so four fit (measured at the Llama-3.1 point, 512 units: one wave instead of
+// 1.73); otherwise 512 threads (Qwen2.5's 256 units of 100k candidates: 256 threads were slower,
+// 182 -> 220 us).  TC: the tie list (keys of the cutoff bin kept in shared memory).
 
 __device__ __forceinline__ float bf16_to_f32(uint16_t b) { return __uint_as_float(static_cast<uint32_t>(b) << 16); }
 
@@ -361,26 +361,27 @@ __device__ __forceinline__ void find_cut(const uint32_t* hist, int nb, uint32_t 
 }
 
 // One CTA per unit.  The pass-1 histogram (10-bit top digit) comes from the score kernel.
-// The candidate scores are staged in shared memory by one bulk copy per super-block of SB
+// The candidate scores are staged in shared memory by one bulk copy per super-block of NT * RL
 // candidates; thread t owns the contiguous run [t*RL, (t+1)*RL) of it (RL = 36: the 16-byte
 // loads of 8 consecutive threads hit disjoint banks).  Pass over the runs: count the keys above
 // the cutoff bin and gather the cutoff bin's keys (with their owner thread) into a small list;
 // passes 2-3 (11 + 11 bits) refine the threshold key thr and how many keys equal to thr to
 // take (the lowest positions) on that list, which also yields every thread's count of
 // selected keys; an exclusive scan of the counts then places each run's selections in
-// position order (second pass over the runs).  A cutoff bin with more than TIE_CAP keys is
+// position order (second pass over the runs).  A cutoff bin with more than TC keys is
 // refined from global memory instead.
-__global__ void __launch_bounds__(SEL_THREADS, 2) pq_select_kernel(const int32_t* __restrict__ scores,
+template <int NT, int TC>
+__global__ void __launch_bounds__(NT, 1024 / NT) pq_select_kernel(const int32_t* __restrict__ scores,
                                                                    int score_stride, const uint32_t* __restrict__ hist_g,
                                                                    const int32_t* __restrict__ kv_len, int Hkv, int sink,
                                                                    int window, int budget, int32_t* __restrict__ idx,
                                                                    int idx_stride, int32_t* __restrict__ idx_count,
                                                                    int32_t* __restrict__ tail_start) {
-  extern __shared__ __align__(16) int32_t stage[];  // [SB] staged scores, ties[TIE_CAP], owner[TIE_CAP]
-  uint32_t* ties = reinterpret_cast<uint32_t*>(stage + SB);
-  uint16_t* owner = reinterpret_cast<uint16_t*>(ties + TIE_CAP);
+  extern __shared__ __align__(16) int32_t stage[];  // [(NT * RL)] staged scores, ties[TC], owner[TC]
+  uint32_t* ties = reinterpret_cast<uint32_t*>(stage + NT * RL);
+  uint16_t* owner = reinterpret_cast<uint16_t*>(ties + TC);
   __shared__ uint32_t hist[HIST2];
-  __shared__ uint32_t n_gt_sm[SEL_THREADS], n_eq_sm[SEL_THREADS];
+  __shared__ uint32_t n_gt_sm[NT], n_eq_sm[NT];
   __shared__ uint32_t scan_sm[65];
   __shared__ __align__(8) uint64_t bar;
   __shared__ int s_bin;
@@ -398,18 +399,18 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) pq_select_kernel(const int32_t
     idx_count[b] = s0 + c;
     tail_start[b] = tail;
   }
-  for (int j = threadIdx.x; j < s0; j += SEL_THREADS) out[j] = j;
+  for (int j = threadIdx.x; j < s0; j += NT) out[j] = j;
   if (c == 0) return;
   out += s0;
   if (c == cnt) {  // the budget covers every candidate
-    for (int j = threadIdx.x; j < cnt; j += SEL_THREADS) out[j] = s0 + j;
+    for (int j = threadIdx.x; j < cnt; j += NT) out[j] = s0 + j;
     return;
   }
   const int32_t* sc = scores + (size_t)unit * score_stride;  // candidate j at sc[j] (16-byte aligned)
   // ---- pass 1 (histogram from the score kernel): cutoff bin of the top digit
   {
     const uint32_t* hg = hist_g + (size_t)unit * HIST1;
-    for (int i = threadIdx.x; i < HIST1; i += SEL_THREADS) hist[i] = __ldcg(hg + i);
+    for (int i = threadIdx.x; i < HIST1; i += NT) hist[i] = __ldcg(hg + i);
     if (threadIdx.x == 0) {
       s_nties = 0;
       mbar_init(&bar, 1);
@@ -417,15 +418,15 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) pq_select_kernel(const int32_t
     }
     __syncthreads();
   }
-  find_cut<SEL_THREADS>(hist, HIST1, (uint32_t)c, scan_sm, &s_bin, &s_need);
+  find_cut<NT>(hist, HIST1, (uint32_t)c, scan_sm, &s_bin, &s_need);
   const uint32_t cb = (uint32_t)s_bin;
   uint32_t prefix = cb << 22, need = s_need;
   const uint32_t nbin = hist[cb];
-  const bool gathered = nbin <= TIE_CAP;
-  const int nsb = (cnt + SB - 1) / SB;
+  const bool gathered = nbin <= TC;
+  const int nsb = (cnt + (NT * RL) - 1) / (NT * RL);
   uint32_t phase = 0;
-  auto stage_block = [&](int base) {  // candidates [base, base + SB) -> stage (one bulk copy)
-    const int nb = min(SB, cnt - base);
+  auto stage_block = [&](int base) {  // candidates [base, base + (NT * RL)) -> stage (one bulk copy)
+    const int nb = min((NT * RL), cnt - base);
     __syncthreads();  // every reader of the previous super-block is done
     if (threadIdx.x == 0) {
       fence_proxy_async();  // earlier generic reads of the stage before the async-proxy overwrite
@@ -456,12 +457,12 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) pq_select_kernel(const int32_t
   // ---- runs pass 1: keys of the cutoff bin -> ties (with their owner thread)
   if (gathered) {
     for (int sb = 0; sb < nsb; ++sb) {
-      const int nb = stage_block(sb * SB);
+      const int nb = stage_block(sb * (NT * RL));
       for_run(nb, [&](int, uint32_t kk) {
         if ((kk >> 22) == cb) {
           const uint32_t slot = atomicAdd(&s_nties, 1u);
           ties[slot] = kk;
-          owner[slot] = (uint16_t)(sb * SEL_THREADS + threadIdx.x);
+          owner[slot] = (uint16_t)(sb * NT + threadIdx.x);
         }
       });
     }
@@ -472,21 +473,21 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) pq_select_kernel(const int32_t
   for (int d = 0; d < 2; ++d) {
     const int sh = d == 0 ? 11 : 0;
     const uint32_t hi_mask = 0xffffffffu << (sh + 11);
-    for (int i = threadIdx.x; i < HIST2; i += SEL_THREADS) hist[i] = 0;
+    for (int i = threadIdx.x; i < HIST2; i += NT) hist[i] = 0;
     __syncthreads();
     if (gathered) {
-      for (int j = threadIdx.x; j < (int)nbin; j += SEL_THREADS) {
+      for (int j = threadIdx.x; j < (int)nbin; j += NT) {
         const uint32_t kk = ties[j];
         if ((kk & hi_mask) == prefix) atomicAdd(&hist[(kk >> sh) & (HIST2 - 1)], 1u);
       }
     } else {
-      for (int j = threadIdx.x; j < cnt; j += SEL_THREADS) {
+      for (int j = threadIdx.x; j < cnt; j += NT) {
         const uint32_t kk = okey(__ldcg(sc + j));
         if ((kk & hi_mask) == prefix) atomicAdd(&hist[(kk >> sh) & (HIST2 - 1)], 1u);
       }
     }
     __syncthreads();
-    find_cut<SEL_THREADS>(hist, HIST2, need, scan_sm, &s_bin, &s_need);
+    find_cut<NT>(hist, HIST2, need, scan_sm, &s_bin, &s_need);
     prefix |= (uint32_t)s_bin << sh;
     need = s_need;
     __syncthreads();
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) pq_select_kernel(const int32_t
   // ---- runs pass 2: ordered compaction, super-block by super-block
   uint32_t base_out = 0, eq_seen = 0;
   for (int sb = 0; sb < nsb; ++sb) {
-    const int nb = (nsb > 1 || !gathered) ? stage_block(sb * SB) : min(SB, cnt);
+    const int nb = (nsb > 1 || !gathered) ? stage_block(sb * (NT * RL)) : min((NT * RL), cnt);
     uint32_t n_gt = 0, n_eq = 0;
     if (gathered) {
       // counts of this super-block's runs from the tie list: keys above the cutoff bin are
@@ -503,9 +504,9 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) pq_select_kernel(const int32_t
       n_gt_sm[threadIdx.x] = 0;
       n_eq_sm[threadIdx.x] = 0;
       __syncthreads();
-      for (int j = threadIdx.x; j < (int)nbin; j += SEL_THREADS) {
-        const int o = owner[j] - sb * SEL_THREADS;
-        if (o >= 0 && o < SEL_THREADS) {
+      for (int j = threadIdx.x; j < (int)nbin; j += NT) {
+        const int o = owner[j] - sb * NT;
+        if (o >= 0 && o < NT) {
           if (ties[j] > thr) atomicAdd(&n_gt_sm[o], 1u);
           else if (ties[j] == thr) atomicAdd(&n_eq_sm[o], 1u);
         }
@@ -521,11 +522,11 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) pq_select_kernel(const int32_t
       });
     }
     uint32_t tot_eq, tot_gt;
-    const uint32_t eq_before = eq_seen + block_excl_scan<SEL_THREADS>(n_eq, scan_sm, tot_eq);
-    const uint32_t gt_before = block_excl_scan<SEL_THREADS>(n_gt, scan_sm, tot_gt);
+    const uint32_t eq_before = eq_seen + block_excl_scan<NT>(n_eq, scan_sm, tot_eq);
+    const uint32_t gt_before = block_excl_scan<NT>(n_gt, scan_sm, tot_gt);
     uint32_t pos = base_out + gt_before + min(eq_before, take_eq) - min(eq_seen, take_eq);
     uint32_t eq_rank = eq_before;
-    const int base = s0 + sb * SB;
+    const int base = s0 + sb * (NT * RL);
     for_run(nb, [&](int k, uint32_t kk) {
       const bool eq = kk == thr;
       const bool take = kk > thr || (eq && eq_rank < take_eq);
@@ -633,8 +634,10 @@ extern "C" MD_API md_status md_pq_select(const void* q, int32_t batch, int32_t n
   if (done_dev != dev) {
     if (cudaFuncSetAttribute(pq::pq_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pq::SCORE_SMEM) !=
             cudaSuccess ||
-        cudaFuncSetAttribute(pq::pq_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pq::SEL_SMEM) !=
-            cudaSuccess)
+        cudaFuncSetAttribute(pq::pq_select_kernel<512, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             pq::sel_smem(512, 2048)) != cudaSuccess ||
+        cudaFuncSetAttribute(pq::pq_select_kernel<256, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             pq::sel_smem(256, 1024)) != cudaSuccess)
       return check_launch("cudaFuncSetAttribute");
     done_dev = dev;
   }
@@ -647,8 +650,13 @@ extern "C" MD_API md_status md_pq_select(const void* q, int32_t batch, int32_t n
              (int)code_capacity, (const float*)lutf, (const float*)lutmax, kv_len, (int)num_kv_heads, (int)sink, (int)window, scores,
              sstride, hist);
   if (md_status st = check_launch("pq_score_kernel"); st != MD_OK) return st;
-  launch_pdl(pq::pq_select_kernel, dim3(units), dim3(pq::SEL_THREADS), (size_t)pq::SEL_SMEM, s, (const int32_t*)scores, sstride,
-             (const uint32_t*)hist, kv_len, (int)num_kv_heads, (int)sink, (int)window, (int)budget, idx,
-             (int)idx_stride, idx_count, tail_start);
+  if (units > 2 * device_sm_count())
+    launch_pdl(pq::pq_select_kernel<256, 1024>, dim3(units), dim3(256), (size_t)pq::sel_smem(256, 1024), s,
+               (const int32_t*)scores, sstride, (const uint32_t*)hist, kv_len, (int)num_kv_heads, (int)sink,
+               (int)window, (int)budget, idx, (int)idx_stride, idx_count, tail_start);
+  else
+    launch_pdl(pq::pq_select_kernel<512, 2048>, dim3(units), dim3(512), (size_t)pq::sel_smem(512, 2048), s,
+               (const int32_t*)scores, sstride, (const uint32_t*)hist, kv_len, (int)num_kv_heads, (int)sink,
+               (int)window, (int)budget, idx, (int)idx_stride, idx_count, tail_start);
   return check_launch("pq_select_kernel");
 }

@@ -237,3 +237,26 @@ def test_gpu_pq_against_the_fp64_definition_offgrid():
                 assert abs(exact[x] - thr) <= 2 * sbound.max(), (b, u, x)
     assert ncode_diff <= B * Hkv * 16 * max(lens) * 1e-3
     assert nsel_diff <= 8
+
+
+@pytest.mark.parametrize("ties", [False, True])
+def test_select_many_units_256_thread_variant(ties):
+    """More units than one wave of 512-thread select CTAs (2 per SM): the 256-thread variant with
+    the 1024-key tie list (4 CTAs per SM).  ties=True: every unit's scores tie except a few keys,
+    so the cutoff bin overflows the tie list and the global-memory refinement runs."""
+    B, Hq, Hkv, d = 40, 32, 8, 128
+    units = B * Hkv
+    assert units > 2 * torch.cuda.get_device_properties(0).multi_processor_count
+    rng = np.random.default_rng(77 + ties)
+    lens = list(rng.integers(900, 2600, size=B))
+    case = AttnCase(B, Hq, Hkv, d, max(lens) + 8, lens, seed=78, regime=S.Regime("peaky", sink=4)).to_cuda()
+    cb = _codebook(case, lens, rng)
+    q_bits = _rand_bf16(rng, case.qd_bits.shape, 1.0)
+    if ties:
+        codes_np = np.zeros((B, Hkv, max(lens), 16), np.uint8)
+        codes_np[:, :, 300:305] = 9
+    else:
+        codes_np = PQ.pq_encode_cache(case.k_bits, cb, np.zeros(B, np.int64), max(lens))
+    codes_t = torch.from_numpy(np.pad(codes_np, ((0, 0), (0, 0), (0, 8), (0, 0)))).cuda()
+    idx, cnt, tail = _select_gpu(case, q_bits, cb, codes_t, 4, 252, 508, max(lens))
+    _check_select(case, q_bits, cb, codes_np, idx, cnt, tail, 4, 252, 508)
