@@ -485,6 +485,15 @@ __device__ __forceinline__ void trace_stamp(const AttnParams& p, int k) {
 __device__ __forceinline__ int64_t out_row(const AttnParams& p, int b, int kvh, int r) {
   return (int64_t)(b * p.T + r / p.g) * p.Hq + kvh * p.g + r % p.g;
 }
+// row j of a group of consecutive units starting at gu0 (unit gu0 + j / R, its row j % R) in the
+// [B][T][Hq] layout of q / out; drafts (T = 1, R = g): row rr of unit u is u * g + rr, so the
+// group's rows are contiguous and need no integer divisions
+__device__ __forceinline__ int64_t group_row(const AttnParams& p, int gu0, int j) {
+  if (p.T == 1) return (int64_t)gu0 * p.g + j;
+  const int su = j / p.R, r = j - su * p.R;
+  const int bb = (gu0 + su) / p.Hkv, hh = gu0 + su - bb * p.Hkv;
+  return out_row(p, bb, hh, r);
+}
 // row of query row r of unit (b, kvh) in the output layout (local heads, or the TP full-head layout)
 __device__ __forceinline__ int64_t o_row(const AttnParams& p, int b, int kvh, int r) {
   return (int64_t)(b * p.T + r / p.g) * p.out_hq + p.out_h0 + kvh * p.g + r % p.g;
@@ -1112,6 +1121,9 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
 #ifndef MD_EXP_FMA
 #define MD_EXP_FMA 0  // experiment (A/B builds only): R <= 4 draft segments on CUDA-core FMA (fma_segment)
 #endif
+#ifndef MD_EXP_EPI
+#define MD_EXP_EPI 0  // experiment (A/B builds only): keys kernel skips 1 = all output stores, 2 = lse, 3 = out
+#endif
 #ifndef MD_EXP_NOMATH
 #define MD_EXP_NOMATH 0  // experiment (A/B builds only): the keys kernel skips its tile math
 #endif
@@ -1460,11 +1472,8 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   trace_stamp(p, 1);
   if (stashed && warp == NC && lane == 0 && q0_ng > 0) {  // the first group's Q rows into slot 0
     mbar_arrive_expect_tx(&qfull[0], q0_ng * p.R * D * 2);
-    for (int su = 0; su < q0_ng; ++su) {
-      const int bb = (q0_unit + su) / p.Hkv, hh = q0_unit + su - bb * p.Hkv;
-      for (int r = 0; r < p.R; ++r)
-        bulk_load(qbuf + (su * p.R + r) * C::QSTR, p.q + out_row(p, bb, hh, r) * D, D * 2, &qfull[0]);
-    }
+    for (int j = 0; j < q0_ng * p.R; ++j)
+      bulk_load(qbuf + j * C::QSTR, p.q + group_row(p, q0_unit, j) * D, D * 2, &qfull[0]);
     if (p.trace != nullptr) trace_put(p, 14, globaltimer());
   }
   // Unit-aligned plan (draft calls): CTA c owns the whole units [c*U/G, (c+1)*U/G), G = gridDim.x,
@@ -1568,12 +1577,8 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         const int qs = qi & 1;
         mbar_wait(&qempty[qs], ((qi >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&qfull[qs], ng * p.R * D * 2);
-        for (int su = 0; su < ng; ++su) {
-          const int bb = (gu0 + su) / p.Hkv, hh = gu0 + su - bb * p.Hkv;
-          for (int r = 0; r < p.R; ++r)
-            bulk_load(qbuf + (qs * C::ROWS + su * p.R + r) * C::QSTR, p.q + out_row(p, bb, hh, r) * D, D * 2,
-                      &qfull[qs]);
-        }
+        for (int j = 0; j < ng * p.R; ++j)
+          bulk_load(qbuf + (qs * C::ROWS + j) * C::QSTR, p.q + group_row(p, gu0, j) * D, D * 2, &qfull[qs]);
         if (qi == 0 && p.trace != nullptr) trace_put(p, 14, globaltimer());
       }
       __syncwarp();
@@ -1848,12 +1853,21 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         const float4 a = *reinterpret_cast<const float4*>(obuf + r * D + sc);
         const float4 c = *reinterpret_cast<const float4*>(obuf + FRAG + r * D + sc);
         const float4 v = make_float4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
-        if (complete) {
+        if (MD_EXP_EPI == 1) {  // experiment: no output stores (bound of their cost)
+          if (v.x == 12345.f) p.out[0] = v.y;
+        } else if (MD_EXP_EPI != 4 && complete && p.T == 1 && p.out_peers == nullptr) {
+          // drafts (T = 1, R = g): row rr of unit u is output row u * g + rr, so the group's rows are
+          // the contiguous rows gu0 * g + r -- no integer divisions on the store path
+          const int64_t orow = group_row(p, gu0, r);
+          if (MD_EXP_EPI != 3) *reinterpret_cast<float4*>(p.out + orow * D + c4) = v;
+          if (MD_EXP_EPI != 2 && c4 == 0 && p.lse != nullptr) p.lse[orow] = lsebuf[r] * LN2;
+        } else if (complete) {
           // row r of the group = row r % R of unit gu0 + r / R (one unit: gu0 = sg.unit)
           const int su = r / p.R, rr = r - su * p.R;
           const int bb = (gu0 + su) / p.Hkv, hh = gu0 + su - bb * p.Hkv;
-          store_out(p, o_row(p, bb, hh, rr) * D + c4, v);
-          if (c4 == 0 && p.lse != nullptr) p.lse[out_row(p, bb, hh, rr)] = lsebuf[r] * LN2;
+          if (MD_EXP_EPI != 3) store_out(p, o_row(p, bb, hh, rr) * D + c4, v);
+          else if (v.x == 12345.f) p.out[0] = v.y;
+          if (MD_EXP_EPI != 2 && c4 == 0 && p.lse != nullptr) p.lse[out_row(p, bb, hh, rr)] = lsebuf[r] * LN2;
         } else {
           const int64_t prow = (int64_t)slot_base * p.R + r;
           __stcg(reinterpret_cast<float4*>(p.ws_o + prow * D + c4), v);
