@@ -1414,12 +1414,16 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   // after the release (griddepcontrol.wait makes the L1 reload it: ~2 us under a saturated fabric),
   // and the producer issues the first group's Q loads as its first action after the release
   const bool stashed = EARLY && MD_DIRECT_UNITS && p.unit_aligned && p.early_kv;
-  const int stash_b0 = (int)((int64_t)blockIdx.x * (p.B * p.Hkv) / gridDim.x) / p.Hkv;
+  // this CTA's units of the unit-aligned plan, [cu0, cu1) = [c U / G, (c + 1) U / G), in 32-bit
+  // unsigned arithmetic (c < G and U <= MAX_UNITS = 2^16: the products stay below 2^32) -- computed
+  // once, before the grid-dependency wait (64-bit divisions cost ~0.1 us each on the start-up path)
+  const unsigned cu0 = (unsigned)blockIdx.x * (unsigned)(p.B * p.Hkv) / gridDim.x;
+  const unsigned cu1 = ((unsigned)blockIdx.x + 1u) * (unsigned)(p.B * p.Hkv) / gridDim.x;
+  const int stash_b0 = (int)cu0 / p.Hkv;
   int q0_unit = -1, q0_ng = 0;  // producer lane 0: the first group, whose Q loads go out right after the wait
   if (stashed) {
     if (warp == NC) {
-      const int U0 = p.B * p.Hkv, G0 = gridDim.x;
-      const int u0 = (int)((int64_t)blockIdx.x * U0 / G0), u1 = (int)((int64_t)(blockIdx.x + 1) * U0 / G0);
+      const int u0 = (int)cu0, u1 = (int)cu1;
       const int nb = u1 > u0 ? (u1 - 1) / p.Hkv - stash_b0 + 1 : 0;
       for (int i = lane; i < nb; i += 32) pre[i] = __ldg(p.kv_len + stash_b0 + i);
     }
@@ -1430,9 +1434,8 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     }
     __syncthreads();  // the barrier initialisation, the plan and the stash are visible to every warp
     if (warp == NC) {
-      const int U0 = p.B * p.Hkv, G0 = gridDim.x;
       SegWalker w0;
-      w0.init_units((int)((int64_t)blockIdx.x * U0 / G0), (int)((int64_t)(blockIdx.x + 1) * U0 / G0), pre, stash_b0);
+      w0.init_units((int)cu0, (int)cu1, pre, stash_b0);
       Seg s0;
       if (w0.next(p, pre, s0)) {
         q0_unit = s0.unit;
@@ -1503,7 +1506,8 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   const int U = p.B * p.Hkv;
   auto init_walk = [&](SegWalker& w) {
     if (direct) {
-      w.init_units((int)((int64_t)chunk * U / pl.G), (int)((int64_t)(chunk + 1) * U / pl.G), stashed ? pre : nullptr,
+      // (chunk == blockIdx.x and pl.G == gridDim.x in the unit-aligned plan: no dynamic chunks)
+      w.init_units((int)cu0, (int)cu1, stashed ? pre : nullptr,
                    stash_b0);
     } else {
       int64_t S0, E0;
