@@ -1660,13 +1660,16 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     // new-key visibility of the two rows 2cq, 2cq+1 this thread holds (verify; rows past R
     // take the mask of row R-1, their output is dropped)
     const int vbase = (p.mode == MODE_VERIFY) ? n - p.T : 0x7fffffff;
-    uint32_t msk[2];
+    uint32_t msk[2] = {~0u, ~0u};
+    if (p.mode == MODE_VERIFY) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) msk[j] = node_mask(p, sg.b, 2 * cq + j);
-    // packed group: rows 2cq, 2cq+1 take part in this unit's tiles only if they are its rows
+      for (int j = 0; j < 2; ++j) msk[j] = node_mask(p, sg.b, 2 * cq + j);
+    }
+    // packed group: rows 2cq, 2cq+1 take part in this unit's tiles only if they are its rows,
+    // [su R, su R + R) (no division: this runs at every sub-unit start)
     bool act[2];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) act[j] = p.pack == 1 || (2 * cq + j) / p.R == su;
+    for (int j = 0; j < 2; ++j) act[j] = p.pack == 1 || (unsigned)(2 * cq + j - su * p.R) < (unsigned)p.R;
     const bool packed = p.pack > 1;
 
 #pragma unroll 1
@@ -1848,7 +1851,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     trace_stamp(p, 7);
     // rows r < R -> the final output, or this CTA's partial slot
     const bool complete = sg.complete();
-    const int slot_base = seg_slot(p, pl, sg, chunk);
+    const int slot_base = complete ? 0 : seg_slot(p, pl, sg, chunk);  // (a 64-bit division: split segments only)
     {
       constexpr int V4 = D / 4;
       for (int idx = threadIdx.x; idx < ng * p.R * V4; idx += NC * 32) {
