@@ -135,7 +135,7 @@ om = tokens / steps / B
 print(json.dumps({
     "workload": "paper Table (P:531-545): Llama-3.1-8B GQA 32/8, d=128, prefill 100k, batch 41, SnapKV draft "
                 f"(window {w}, pooling 5, budget {budget}), gamma {gamma}, 32 layers (4 rotated 16.8 GB caches)",
-    "metric": "spec-step tokens/s (attention-only hot path)", "value": round(tokens / (ms / 1e3), 1),
+    "metric": "spec-step tokens/s (attention-only hot path)", "value": round(tokens / steps / (ms / 1e3), 1),
     "ms_per_step": round(ms, 3), "steps": steps, "tokens_per_step": round(tokens / steps, 1),
     "beta_mean": round(float(beta.mean()), 4), "alpha_implied_by_measured_omega": round(alpha_from_omega(gamma, om), 4),
     "verify_ms": round(v_ms, 4), "verify_gbs": round(vb / v_ms / 1e6, 1), "verify_rows_per_kv_head": 4 * T,
