@@ -4,9 +4,9 @@
 // products (m * q < p * 2^29, m = rnd >> 3: 29 x 24 bits fit in the 53-bit mantissa),
 // then draws the final token from an integer weight vector on the 2^-40 grid with a
 // 64-bit uniform.  All sums are uint64 (<= V * 2^40 < 2^58), so the result does not
-// depend on the reduction order and is bit-identical to the oracle's.  Each thread owns
-// a contiguous slice of the vocabulary row (8-deep batched loads); a block exclusive scan
-// of the slice sums locates the slice holding the draw, which one thread rescans.
+// depend on the reduction order and is bit-identical to the oracle's.  Each warp streams a
+// contiguous segment of the vocabulary row with coalesced, 8-chunk-deep loads; a scan of the
+// segment sums locates the segment holding the draw, which the block re-streams (see below).
 #include "md_common.cuh"
 #include "md_internal.h"
 
@@ -80,100 +80,183 @@ struct Smem {
   int n;
 };
 
-// Thread tid owns the contiguous slice [tid*chunk, min(V, (tid+1)*chunk)) of the row, so
-// an exclusive scan of the per-thread sums gives every slice's starting prefix and the
-// locate step is one thread rescanning one slice.  Loads are batched 8 deep per thread
-// (memory-level parallelism; the row is read once from HBM).
-constexpr int UNR = 8;
+// Warp-strip layout (round 2): the row is cut into ACC_WARPS contiguous warp segments whose
+// lengths are multiples of one warp chunk (CH = 32 * VEC elements); a warp streams its segment
+// chunk by chunk, lane l taking elements [c + l * VEC, c + l * VEC + VEC) -- coalesced 16-byte
+// loads (VEC = 4) when both rows are 16-byte aligned, 4-byte loads otherwise -- BATCH chunks
+// in flight.  A block scan of the warp sums gives every segment's prefix; the locate step
+// re-streams the one segment holding the draw with the whole block (sub-segments per warp),
+// and one warp walks its sub-segment chunk by chunk with a lane scan.  Every sum is an exact
+// uint64, so the token (min{k : sum_{i<=k} W_i > t}) is the same as any other order's.
+// (The round-1 layout -- thread t owns the contiguous slice [t V/512, ...) read with 4-byte
+// loads -- touched 32 sectors per warp load instruction and ran at ~1 TB/s.)
+constexpr int BATCH = 4;  // chunks in flight per warp (x 2 rows x 16 B x 32 lanes)
 
-__device__ __forceinline__ uint64_t slice_sum(const float* __restrict__ prow, const float* __restrict__ qrow, int beg,
-                                              int end) {
-  uint64_t acc = 0;
-  int i = beg;
-  for (; i + UNR <= end; i += UNR) {
-    float pv[UNR], qv[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) pv[u] = __ldg(prow + i + u);
-    if (qrow != nullptr) {
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) qv[u] = __ldg(qrow + i + u);
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const uint64_t P = grid40(pv[u]);
-      const uint64_t Q = qrow != nullptr ? grid40(qv[u]) : 0ull;
-      acc += P > Q ? P - Q : 0ull;
+__device__ __forceinline__ uint64_t wdiff(float p, float q) {
+  const uint64_t P = grid40(p), Q = grid40(q);
+  return P > Q ? P - Q : 0ull;
+}
+
+// weights of the VEC elements [i, i + VEC) (0 past V)
+template <int VEC>
+__device__ __forceinline__ void chunk_weights(const float* __restrict__ prow, const float* __restrict__ qrow, int i,
+                                              int V, uint64_t (&w)[VEC]) {
+  if constexpr (VEC == 4) {
+    if (i + 3 < V) {
+      const float4 pv = __ldg(reinterpret_cast<const float4*>(prow + i));
+      const float4 qv = qrow != nullptr ? __ldg(reinterpret_cast<const float4*>(qrow + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      w[0] = wdiff(pv.x, qv.x);
+      w[1] = wdiff(pv.y, qv.y);
+      w[2] = wdiff(pv.z, qv.z);
+      w[3] = wdiff(pv.w, qv.w);
+      return;
     }
   }
-  for (; i < end; ++i) acc += weight(prow, qrow, i);
+#pragma unroll
+  for (int u = 0; u < VEC; ++u) w[u] = (i + u < V) ? weight(prow, qrow, i + u) : 0ull;
+}
+
+// sum of the weights of [beg, end) (beg a multiple of CH relative to the row, end <= V) by one warp;
+// every lane returns the total.  The BATCH chunks' loads are issued before any weight is formed.
+template <int VEC>
+__device__ uint64_t warp_range_sum(const float* __restrict__ prow, const float* __restrict__ qrow, int beg, int end,
+                                   int V) {
+  constexpr int CH = 32 * VEC;
+  const int lane = threadIdx.x & 31;
+  uint64_t acc = 0;
+  for (int c0 = beg; c0 < end; c0 += CH * BATCH) {
+    float pv[BATCH][VEC], qv[BATCH][VEC];
+#pragma unroll
+    for (int k = 0; k < BATCH; ++k) {
+      const int i = c0 + k * CH + lane * VEC;
+      if constexpr (VEC == 4) {
+        if (i + 3 < end) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(prow + i));
+          const float4 c = qrow != nullptr ? __ldg(reinterpret_cast<const float4*>(qrow + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          pv[k][0] = a.x; pv[k][1] = a.y; pv[k][2] = a.z; pv[k][3] = a.w;
+          qv[k][0] = c.x; qv[k][1] = c.y; qv[k][2] = c.z; qv[k][3] = c.w;
+          continue;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) {  // 4-byte loads (VEC = 1), the row's last partial chunk, or past the end
+        const bool in = i + u < end;
+        pv[k][u] = in ? __ldg(prow + i + u) : 0.f;
+        qv[k][u] = (in && qrow != nullptr) ? __ldg(qrow + i + u) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < BATCH; ++k)
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) acc += wdiff(pv[k][u], qv[k][u]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return acc;
 }
 
-// Per-thread slice sums -> exclusive prefix (returned) and the block total in sm.total.
-__device__ uint64_t block_weight_scan(const float* prow, const float* qrow, int V, int chunk, Smem& sm,
-                                      uint64_t& mine) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int beg = min(V, tid * chunk), end = min(V, beg + chunk);
-  mine = slice_sum(prow, qrow, beg, end);
-  uint64_t incl = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t up = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += up;
+__device__ __forceinline__ int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Pass 1: warp segment sums -> sm.wsum, sm.total.
+template <int VEC>
+__device__ void block_weight_sums(const float* prow, const float* qrow, int V, Smem& sm) {
+  constexpr int CH = 32 * VEC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seg = round_up((V + ACC_WARPS - 1) / ACC_WARPS, CH);
+  const int beg = min(V, warp * seg), end = min(V, beg + seg);
+  const uint64_t s = warp_range_sum<VEC>(prow, qrow, beg, end, V);
+  __syncthreads();  // sm.wsum may still be read by a previous pass
+  if (lane == 0) sm.wsum[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t total = 0;
+    for (int w = 0; w < ACC_WARPS; ++w) total += sm.wsum[w];
+    sm.total = total;
   }
   __syncthreads();
-  if (lane == 31) sm.wsum[warp] = incl;
-  __syncthreads();
-  uint64_t before = 0, total = 0;
-  for (int w = 0; w < ACC_WARPS; ++w) {
-    const uint64_t v = sm.wsum[w];
-    if (w < warp) before += v;
-    total += v;
-  }
-  if (tid == 0) sm.total = total;
-  return before + incl - mine;
 }
 
-// token = min{k : sum_{i<=k} W_i > t}: the one thread whose slice straddles t rescans it.
-__device__ int block_locate(const float* prow, const float* qrow, int V, int chunk, uint64_t t, uint64_t pre,
-                            uint64_t mine, Smem& sm) {
-  const int tid = threadIdx.x;
-  if (mine != 0 && pre <= t && t < pre + mine) {
-    const int beg = tid * chunk, end = min(V, beg + chunk);
-    uint64_t run = pre;
-    int i = beg;
-    for (; i + UNR <= end; i += UNR) {
-      uint64_t w[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) w[u] = weight(prow, qrow, i + u);
-      uint64_t blk = 0;
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) blk += w[u];
-      if (run + blk > t) {
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          run += w[u];
-          if (run > t) {
-            sm.token = i + u;
-            break;
-          }
-        }
-        i = end + 1;  // found
-        break;
-      }
-      run += blk;
+// token = min{k : sum_{i<=k} W_i > t}, t < sm.total (after block_weight_sums).
+template <int VEC>
+__device__ int block_locate(const float* prow, const float* qrow, int V, uint64_t t, Smem& sm) {
+  constexpr int CH = 32 * VEC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seg = round_up((V + ACC_WARPS - 1) / ACC_WARPS, CH);
+  // the warp segment holding t (every thread finds the same one)
+  uint64_t run = 0;
+  int ws = 0;
+  for (int w = 0; w < ACC_WARPS; ++w) {
+    const uint64_t v = sm.wsum[w];
+    if (run + v > t) {
+      ws = w;
+      break;
     }
-    for (; i < end; ++i) {
-      run += weight(prow, qrow, i);
-      if (run > t) {
-        sm.token = i;
+    run += v;
+  }
+  const int base = min(V, ws * seg), send = min(V, base + seg);
+  // its sub-segments, one per warp
+  const int sub = round_up((send - base + ACC_WARPS - 1) / ACC_WARPS, CH);
+  const int sbeg = min(send, base + warp * sub), send2 = min(send, sbeg + sub);
+  const uint64_t s = warp_range_sum<VEC>(prow, qrow, sbeg, send2, V);
+  __syncthreads();  // every warp has read sm.wsum
+  if (lane == 0) sm.wsum[warp] = s;
+  __syncthreads();
+  int w2 = 0;
+  for (int w = 0; w < ACC_WARPS; ++w) {
+    const uint64_t v = sm.wsum[w];
+    if (run + v > t) {
+      w2 = w;
+      break;
+    }
+    run += v;
+  }
+  if (warp == w2) {  // walk this warp's sub-segment chunk by chunk
+    const int b2 = min(send, base + w2 * sub), e2 = min(send, b2 + sub);
+    for (int c0 = b2; c0 < e2; c0 += CH) {
+      uint64_t w[VEC];
+      const int i = c0 + lane * VEC;
+      if (i < e2) {
+        chunk_weights<VEC>(prow, qrow, i, V, w);
+      } else {
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) w[u] = 0ull;
+      }
+      uint64_t ls = 0;
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) ls += w[u];
+      uint64_t incl = ls;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t up = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += up;
+      }
+      const uint64_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (run + tot > t) {
+        const unsigned hit = __ballot_sync(0xffffffffu, run + incl > t);
+        const int L = __ffs(hit) - 1;
+        if (lane == L) {
+          uint64_t r = run + incl - ls;
+          int k = i;
+#pragma unroll
+          for (int u = 0; u < VEC; ++u) {
+            r += w[u];
+            if (r > t) {
+              k = i + u;
+              break;
+            }
+          }
+          sm.token = k;
+        }
         break;
       }
+      run += tot;
     }
   }
   __syncthreads();
   return sm.token;
 }
+
+constexpr int UNR = 8;  // argmax: loads in flight per thread
 
 // Lowest-index argmax of a row (block-wide).  All threads return the same value.
 __device__ int block_argmax(const float* __restrict__ row, int V, Smem& sm) {
@@ -228,7 +311,7 @@ __device__ int block_argmax(const float* __restrict__ row, int V, Smem& sm) {
   return sm.token;
 }
 
-__global__ void __launch_bounds__(ACC_THREADS) spec_accept_kernel(
+__global__ void __launch_bounds__(ACC_THREADS, 2) spec_accept_kernel(
     const float* __restrict__ p, const float* __restrict__ q, const int32_t* __restrict__ dtok,
     const uint32_t* __restrict__ rnd, int gamma, int V, int mode, int32_t* __restrict__ out_tokens,
     int32_t* __restrict__ num_accepted, int32_t* __restrict__ committed_len) {
@@ -239,7 +322,6 @@ __global__ void __launch_bounds__(ACC_THREADS) spec_accept_kernel(
   const int64_t Vl = V;
   const float* pb = p + (int64_t)b * (gamma + 1) * Vl;
   const int32_t* db = dtok + (int64_t)b * gamma;
-  const int chunk = (V + ACC_THREADS - 1) / ACC_THREADS;
   int n, token;
   if (mode == MD_ACCEPT_SAMPLE) {
     const uint32_t* rb = rnd + (int64_t)b * (gamma + 2);
@@ -261,14 +343,15 @@ __global__ void __launch_bounds__(ACC_THREADS) spec_accept_kernel(
     n = sm.n;
     const float* prow = pb + (int64_t)n * Vl;
     const float* qrow = (n < gamma) ? q + ((int64_t)b * gamma + n) * Vl : nullptr;
-    uint64_t mine;
-    uint64_t pre = block_weight_scan(prow, qrow, V, chunk, sm, mine);
-    __syncthreads();
+    // 16-byte loads when both rows are 16-byte aligned (uniform over the CTA)
+    const bool vec = ((reinterpret_cast<uintptr_t>(prow) | reinterpret_cast<uintptr_t>(qrow)) & 15u) == 0;
+    if (vec) block_weight_sums<4>(prow, qrow, V, sm);
+    else block_weight_sums<1>(prow, qrow, V, sm);
     uint64_t total = sm.total;
     if (total == 0 && qrow != nullptr) {  // degenerate residual: fall back to p (reading Z7)
       qrow = nullptr;
-      pre = block_weight_scan(prow, qrow, V, chunk, sm, mine);
-      __syncthreads();
+      if (vec) block_weight_sums<4>(prow, qrow, V, sm);
+      else block_weight_sums<1>(prow, qrow, V, sm);
       total = sm.total;
     }
     if (total == 0) {
@@ -276,7 +359,7 @@ __global__ void __launch_bounds__(ACC_THREADS) spec_accept_kernel(
     } else {
       const uint64_t u = (static_cast<uint64_t>(__ldg(rb + gamma)) << 32) | __ldg(rb + gamma + 1);
       const uint64_t t = __umul64hi(u, total);
-      token = block_locate(prow, qrow, V, chunk, t, pre, mine, sm);
+      token = vec ? block_locate<4>(prow, qrow, V, t, sm) : block_locate<1>(prow, qrow, V, t, sm);
     }
   } else {
     n = gamma;
