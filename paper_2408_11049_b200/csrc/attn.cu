@@ -18,14 +18,19 @@
 // Per CTA: one TMA producer warp (one lane) streams 64-key K and V tiles with 4-D
 // cp.async.bulk.tensor boxes (SWIZZLE_128B, L2 evict_first) into an mbarrier ring — one
 // 64-row box per 128-byte column slab for full tiles, 16-row boxes for ragged ends so
-// only rows holding valid keys are fetched — and NC consumer warps do the math with
-// mma.sync m16n8k16 bf16 -> fp32 (HMMA; ~550 TFLOP/s measured on this B200, far above the
-// <= 48 FLOP/B x 7 TB/s this HBM-bound loop needs) and an online softmax in the log2
-// domain.  Two consumer layouts:
-//   attn_rows_kernel  R > 8 query rows per KV head (GQA verify: g*(gamma+1) = 20 / 35):
+// only rows holding valid keys are fetched — and the consumer warps do the math with an
+// online softmax in the log2 domain.  Three kernels:
+//   attn_tc_kernel    (attn_tc.cuh) head_dim 128 verify with 8 < R <= 128 query rows per KV
+//                     head (GQA verify: g*(gamma+1) = 20 / 35 ...): tcgen05 MMAs, S^T and O^T in
+//                     TMEM, one CTA / SM.
+//   attn_rows_kernel  head_dim 64 verify with R > 8, drafts with g > 8: mma.sync m16n8k16,
 //                     query rows on the MMA M dimension (16-row tiles); 2 CTAs / SM.
-//   attn_keys_kernel  R <= 8 (every draft call, MHA verify): "swap-AB", 16 KV tokens on
-//                     M and the query rows on N (padded to 8, not 16); 1 CTA / SM.
+//   attn_keys_kernel  R <= 8 (every draft call, MHA verify): mma.sync "swap-AB", 16 KV tokens
+//                     on M and the query rows on N (padded to 8; an A/B with CUDA-core FMA ran
+//                     1.35x slower); 2 CTAs / SM.  Draft calls run the unit-aligned plan (whole
+//                     units per CTA, no merges), pack up to 8 / R units of a CTA into one pass
+//                     (AttnParams::pack), and with MD_ATTN_EARLY_KV stream their first tiles
+//                     (and prefetch the next ones into L2) before the grid-dependency wait.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
