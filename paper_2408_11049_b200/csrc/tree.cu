@@ -78,70 +78,161 @@ struct TreeSmem {
   int accepted;
 };
 
-// Sum over the thread's contiguous slice of resid(stage k), loads batched TR_UNR deep.
-__device__ uint64_t tree_slice_sum(const float* __restrict__ prow, const float* __restrict__ qrow, int beg, int end,
-                                   const TreeHist& h, int k) {
-  uint64_t acc = 0;
-  int i = beg;
-  for (; i + TR_UNR <= end; i += TR_UNR) {
-    float pv[TR_UNR], qv[TR_UNR];
-#pragma unroll
-    for (int u = 0; u < TR_UNR; ++u) pv[u] = __ldg(prow + i + u);
-    if (k >= 0) {
-#pragma unroll
-      for (int u = 0; u < TR_UNR; ++u) qv[u] = __ldg(qrow + i + u);
+// Row scans in the warp-strip layout of spec_accept.cu (round 2): contiguous warp
+// segments streamed with coalesced 16-byte loads (4-byte when a row is not 16-byte aligned),
+// TR_BATCH chunks in flight; the locate step re-streams the segment holding the draw with the
+// whole block and one warp walks its sub-segment with a lane scan.  Weights are exact uint64
+// (resid of stage k), so every sum and the drawn token are independent of the order.
+constexpr int TR_BATCH = 4;
+
+__device__ __forceinline__ uint64_t tw(float pv, float qv, const TreeHist& h, int k) {
+  return resid(tgrid40(pv), k >= 0 ? tgrid40(qv) : 0ull, h, k);
+}
+__device__ __forceinline__ int tr_round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// the VEC floats of p (and q when k >= 0) at [i, i + VEC), zeros past `end`
+template <int VEC>
+__device__ __forceinline__ void tr_load(const float* __restrict__ prow, const float* __restrict__ qrow, int i, int end,
+                                        int k, float (&pv)[VEC], float (&qv)[VEC]) {
+  if constexpr (VEC == 4) {
+    if (i + 3 < end) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(prow + i));
+      const float4 c = k >= 0 ? __ldg(reinterpret_cast<const float4*>(qrow + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      pv[0] = a.x; pv[1] = a.y; pv[2] = a.z; pv[3] = a.w;
+      qv[0] = c.x; qv[1] = c.y; qv[2] = c.z; qv[3] = c.w;
+      return;
     }
-#pragma unroll
-    for (int u = 0; u < TR_UNR; ++u) acc += resid(tgrid40(pv[u]), k >= 0 ? tgrid40(qv[u]) : 0ull, h, k);
   }
-  for (; i < end; ++i) acc += resid(tgrid40(__ldg(prow + i)), k >= 0 ? tgrid40(__ldg(qrow + i)) : 0ull, h, k);
+#pragma unroll
+  for (int u = 0; u < VEC; ++u) {
+    const bool in = i + u < end;
+    pv[u] = in ? __ldg(prow + i + u) : 0.f;
+    qv[u] = (in && k >= 0) ? __ldg(qrow + i + u) : 0.f;
+  }
+}
+
+template <int VEC>
+__device__ uint64_t tr_warp_sum(const float* prow, const float* qrow, int beg, int end, const TreeHist& h, int k) {
+  constexpr int CH = 32 * VEC;
+  const int lane = threadIdx.x & 31;
+  uint64_t acc = 0;
+  for (int c0 = beg; c0 < end; c0 += CH * TR_BATCH) {
+    float pv[TR_BATCH][VEC], qv[TR_BATCH][VEC];
+#pragma unroll
+    for (int b = 0; b < TR_BATCH; ++b) tr_load<VEC>(prow, qrow, c0 + b * CH + lane * VEC, end, k, pv[b], qv[b]);
+#pragma unroll
+    for (int b = 0; b < TR_BATCH; ++b)
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) acc += (c0 + b * CH + lane * VEC + u < end) ? tw(pv[b][u], qv[b][u], h, k) : 0ull;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return acc;
 }
 
-// Block-wide: exclusive prefix of this thread's slice sum (returned), its own sum in `mine`
-// and the total in sm.total.
-__device__ uint64_t tree_scan(const float* prow, const float* qrow, int V, int chunk, TreeSmem& sm, int k,
-                              uint64_t& mine) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int beg = min(V, tid * chunk), end = min(V, beg + chunk);
-  mine = tree_slice_sum(prow, qrow, beg, end, sm.h, k);
-  uint64_t incl = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t up = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += up;
+// warp segment sums of stage k -> sm.wsum, total -> sm.total
+template <int VEC>
+__device__ void tr_sums(const float* prow, const float* qrow, int V, TreeSmem& sm, int k) {
+  constexpr int CH = 32 * VEC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seg = tr_round_up((V + TR_WARPS - 1) / TR_WARPS, CH);
+  const int beg = min(V, warp * seg), end = min(V, beg + seg);
+  const uint64_t s = tr_warp_sum<VEC>(prow, qrow, beg, end, sm.h, k);
+  __syncthreads();
+  if (lane == 0) sm.wsum[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t total = 0;
+    for (int w = 0; w < TR_WARPS; ++w) total += sm.wsum[w];
+    sm.total = total;
   }
   __syncthreads();
-  if (lane == 31) sm.wsum[warp] = incl;
-  __syncthreads();
-  uint64_t before = 0, total = 0;
-  for (int w = 0; w < TR_WARPS; ++w) {
-    const uint64_t v = sm.wsum[w];
-    if (w < warp) before += v;
-    total += v;
-  }
-  if (tid == 0) sm.total = total;
-  __syncthreads();
-  return before + incl - mine;
+}
+__device__ __forceinline__ bool tr_vec_ok(const float* prow, const float* qrow) {
+  return ((reinterpret_cast<uintptr_t>(prow) | reinterpret_cast<uintptr_t>(qrow)) & 15u) == 0;
+}
+__device__ void tree_sums(const float* prow, const float* qrow, int V, TreeSmem& sm, int k) {
+  if (tr_vec_ok(prow, qrow)) tr_sums<4>(prow, qrow, V, sm, k);
+  else tr_sums<1>(prow, qrow, V, sm, k);
 }
 
-// token = min{i : sum_{j<=i} W_j > t}; the thread whose slice straddles t rescans it.
-__device__ int tree_locate(const float* prow, const float* qrow, int V, int chunk, uint64_t t, uint64_t pre,
-                           uint64_t mine, TreeSmem& sm, int k) {
-  const int tid = threadIdx.x;
-  if (mine != 0 && pre <= t && t < pre + mine) {
-    const int beg = tid * chunk, end = min(V, beg + chunk);
-    uint64_t run = pre;
-    for (int i = beg; i < end; ++i) {
-      run += resid(tgrid40(__ldg(prow + i)), k >= 0 ? tgrid40(__ldg(qrow + i)) : 0ull, sm.h, k);
-      if (run > t) {
-        sm.token = i;
+// token = min{i : sum_{j<=i} W_j > t}, t < sm.total (right after tree_sums of the same stage)
+template <int VEC>
+__device__ int tr_locate(const float* prow, const float* qrow, int V, uint64_t t, TreeSmem& sm, int k) {
+  constexpr int CH = 32 * VEC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seg = tr_round_up((V + TR_WARPS - 1) / TR_WARPS, CH);
+  uint64_t run = 0;
+  int ws = 0;
+  for (int w = 0; w < TR_WARPS; ++w) {
+    const uint64_t v = sm.wsum[w];
+    if (run + v > t) {
+      ws = w;
+      break;
+    }
+    run += v;
+  }
+  const int base = min(V, ws * seg), send = min(V, base + seg);
+  const int sub = tr_round_up((send - base + TR_WARPS - 1) / TR_WARPS, CH);
+  const int sbeg = min(send, base + warp * sub), send2 = min(send, sbeg + sub);
+  const uint64_t s = tr_warp_sum<VEC>(prow, qrow, sbeg, send2, sm.h, k);
+  __syncthreads();
+  if (lane == 0) sm.wsum[warp] = s;
+  __syncthreads();
+  int w2 = 0;
+  for (int w = 0; w < TR_WARPS; ++w) {
+    const uint64_t v = sm.wsum[w];
+    if (run + v > t) {
+      w2 = w;
+      break;
+    }
+    run += v;
+  }
+  if (warp == w2) {
+    const int b2 = min(send, base + w2 * sub), e2 = min(send, b2 + sub);
+    for (int c0 = b2; c0 < e2; c0 += CH) {
+      const int i = c0 + lane * VEC;
+      float pv[VEC], qv[VEC];
+      tr_load<VEC>(prow, qrow, i, e2, k, pv, qv);
+      uint64_t w[VEC], ls = 0;
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) {
+        w[u] = (i + u < e2) ? tw(pv[u], qv[u], sm.h, k) : 0ull;
+        ls += w[u];
+      }
+      uint64_t incl = ls;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t up = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += up;
+      }
+      const uint64_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (run + tot > t) {
+        const unsigned hit = __ballot_sync(0xffffffffu, run + incl > t);
+        const int L = __ffs(hit) - 1;
+        if (lane == L) {
+          uint64_t r = run + incl - ls;
+          int tokn = i;
+#pragma unroll
+          for (int u = 0; u < VEC; ++u) {
+            r += w[u];
+            if (r > t) {
+              tokn = i + u;
+              break;
+            }
+          }
+          sm.token = tokn;
+        }
         break;
       }
+      run += tot;
     }
   }
   __syncthreads();
   return sm.token;
+}
+__device__ int tree_locate(const float* prow, const float* qrow, int V, uint64_t t, TreeSmem& sm, int k) {
+  return tr_vec_ok(prow, qrow) ? tr_locate<4>(prow, qrow, V, t, sm, k) : tr_locate<1>(prow, qrow, V, t, sm, k);
 }
 
 __device__ int tree_argmax(const float* __restrict__ row, int V, TreeSmem& sm) {
@@ -197,7 +288,6 @@ __global__ void __launch_bounds__(TR_THREADS) spec_accept_tree_kernel(
   const int32_t* tok = tokens + (int64_t)b * T;
   const int32_t* par = parent + (int64_t)b * T;
   const uint32_t* rb = rnd ? rnd + (int64_t)b * (T + 1) : nullptr;
-  const int chunk = (V + TR_THREADS - 1) / TR_THREADS;
 #ifdef MD_DEBUG
   for (int c = tid; c < T; c += TR_THREADS)  // token ids < V, topological parents (parent[t] < t)
     MD_DCHECK(__ldg(tok + c) >= 0 && __ldg(tok + c) < V && (c == 0 || (__ldg(par + c) >= 0 && __ldg(par + c) < c)));
@@ -257,18 +347,17 @@ __global__ void __launch_bounds__(TR_THREADS) spec_accept_tree_kernel(
       __syncthreads();
       if (sm.accepted >= 0) break;
       // rejected: advance the residual
-      uint64_t mine;
       if (i == 0) {
         if (tid == 0) sm.h.k = 0;
         __syncthreads();
-        tree_scan(prow, qrow, V, chunk, sm, 0, mine);
+        tree_sums(prow, qrow, V, sm, 0);
         if (tid == 0) {
           if (sm.total == 0) sm.h.pfb = 1;
           else sm.h.S[0] = sm.total;
         }
         __syncthreads();
         if (sm.h.pfb) {
-          tree_scan(prow, qrow, V, chunk, sm, 0, mine);
+          tree_sums(prow, qrow, V, sm, 0);
           if (tid == 0) sm.h.S[0] = sm.total;
           __syncthreads();
         }
@@ -278,7 +367,7 @@ __global__ void __launch_bounds__(TR_THREADS) spec_accept_tree_kernel(
         const int k = sm.h.k;
         if (tid == 0) sm.h.keep[k] = 0;
         __syncthreads();
-        tree_scan(prow, qrow, V, chunk, sm, k + 1, mine);  // candidate R^(k+1)
+        tree_sums(prow, qrow, V, sm, k + 1);  // candidate R^(k+1)
         if (tid == 0) {
           sm.h.keep[k] = sm.total == 0;
           sm.h.S[k + 1] = sm.total == 0 ? sm.h.S[k] : sm.total;
@@ -300,14 +389,13 @@ __global__ void __launch_bounds__(TR_THREADS) spec_accept_tree_kernel(
     }
     // ---------------- final draw: from R^(k) (after rejections) or P (leaf)
     const int k = sm.h.k;
-    uint64_t mine;
-    const uint64_t pre = tree_scan(prow, qrow, V, chunk, sm, k, mine);
+    tree_sums(prow, qrow, V, sm, k);
     const uint64_t total = sm.total;
     if (total == 0) {
       token = tree_argmax(prow, V, sm);
     } else {
       const uint64_t u = (static_cast<uint64_t>(__ldg(rb + T - 1)) << 32) | __ldg(rb + T);
-      token = tree_locate(prow, qrow, V, chunk, __umul64hi(u, total), pre, mine, sm, k);
+      token = tree_locate(prow, qrow, V, __umul64hi(u, total), sm, k);
     }
     break;
   }

@@ -51,3 +51,17 @@ res["draft_sampling_only_us"] = round(timed(lambda i: md.spec_accept(q.view(B * 
                                                                      dtok.view(B * gamma, 1), dn, mode="sample")), 1)
 res["bytes_p_q"] = (p.numel() + q.numel()) * 4
 print(json.dumps(res))
+
+# tree acceptance (f3) on a 5-node tree per sequence (root + 2 children + 2 grandchildren under the
+# first child), p / q [B, T, V]: a rejection walks sibling residuals, then the final draw
+T = 5
+pt = torch.softmax(torch.randn((B, T, V), device="cuda", generator=g) * 3, -1).float().contiguous()
+qt = torch.softmax(torch.randn((B, T, V), device="cuda", generator=g) * 3, -1).float().contiguous()
+tok_t = torch.randint(0, V, (B, T), device="cuda", generator=g, dtype=torch.int64).to(torch.int32)
+par_t = torch.tensor([-1, 0, 0, 1, 1], dtype=torch.int32, device="cuda").repeat(B, 1).contiguous()
+rnd_t = torch.randint(0, 2 ** 31 - 1, (B, T + 1), device="cuda", generator=g, dtype=torch.int64).to(torch.int32)
+out_t = torch.zeros((B, T), dtype=torch.int32, device="cuda")
+na_t = torch.zeros(B, dtype=torch.int32, device="cuda")
+res2 = {"tree_accept_us": round(timed(lambda i: md.spec_accept_tree(pt, qt, tok_t, par_t, rnd_t, out_t, na_t)), 1),
+        "tree_T": T, "tree_tokens_sample": out_t[:2].cpu().tolist()}
+print(json.dumps(res2))
