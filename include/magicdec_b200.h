@@ -259,7 +259,8 @@ MD_API md_status md_draft_attn_sparse_append(const md_kv_cache* cache, const voi
  *     the stream without an intervening ordinary kernel, copy, event wait or host synchronisation
  *     (this library's kernels let the next kernel launch early, before they finish; ordinary
  *     work does not).  The kernel may then read kv_len and stream the first key tiles of a unit
- *     (never one holding the appended row, never q) before waiting for the previous kernel, so
+ *     (never one holding the appended row, never q; the next few tiles are also prefetched into
+ *     L2, a hint that is correct regardless) before waiting for the previous kernel, so
  *     the call's ramp overlaps the previous call's tail (a draft step: every layer's call, the
  *     layers' caches distinct from the previous call's).  Results are bit-identical with and
  *     without the flag; without the guarantee the flag is a data race.  Used only where the draft
