@@ -1120,6 +1120,9 @@ __global__ void __launch_bounds__((MT * KS + 1) * 32, 2)
 // 3 best, Llama-3.1 47.2 -> 45.8 us, Qwen2.5 45.4 -> 43.7, B = 128 88.6 -> 87.4; 16+ slower)
 #define MD_EARLY_PF 3
 #endif
+#ifndef MD_EPF_AFTER
+#define MD_EPF_AFTER 0  // experiment (A/B builds only): the early L2 prefetch after the wait and the first Q loads
+#endif
 #ifndef MD_PACK_UNITS
 #define MD_PACK_UNITS 1  // unit packing for R <= 4 drafts (AttnParams::pack; 0: A/B builds)
 #endif
@@ -1156,6 +1159,34 @@ struct KeysCfg {
 #if MD_EXP_FMA
 #include "attn_exp_fma.cuh"  // experiment only: CUDA-core FMA draft consumer (A/B builds)
 #endif
+
+// early-KV draft calls: the next MD_EARLY_PF full tiles of the CTA's units after the NSTAGE issued
+// to shared memory, prefetched into L2 (a hint: safe whatever the previous kernel still writes --
+// L2 is the point of coherence), so the CTAs that become resident during the previous call's tail
+// fill its idle HBM bandwidth with this call's reads.  s0 / w0: the first unit and its walker.
+template <int D>
+__device__ void early_l2_prefetch(const AttnParams& p, const TmapSet& tm, const int* pre, Seg su, SegWalker w0,
+                                  int skip) {
+  int left = MD_EARLY_PF;
+  do {
+    const Ranges rg = seg_ranges(p, su);
+    for (int part = 0; part < 2 && left > 0; ++part) {
+      const int rs = part ? rg.s1 : rg.s0, re = part ? rg.e1 : rg.e0;
+      for (int pos = rs; pos + TK <= re && left > 0; pos += TK) {
+        if (skip > 0) {
+          --skip;
+          continue;
+        }
+        for (int sub = 0; sub < D / 64; ++sub) {
+          tma_prefetch_4d(&tm.k_full, sub * 64, pos, su.kvh, su.b);
+          tma_prefetch_4d(&tm.v_full, sub * 64, pos, su.kvh, su.b);
+        }
+        --left;
+      }
+    }
+    skip = 0;
+  } while (left > 0 && w0.next(p, pre, su));
+}
 
 template <int D, int KS, int CTAS, bool EARLY>
 __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
@@ -1229,6 +1260,8 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
   const unsigned cu1 = ((unsigned)blockIdx.x + 1u) * (unsigned)(p.B * p.Hkv) / gridDim.x;
   const int stash_b0 = (int)cu0 / p.Hkv;
   int q0_unit = -1, q0_ng = 0;  // producer lane 0: the first group, whose Q loads go out right after the wait
+  Seg pf_s0{};                  // (MD_EPF_AFTER: the prefetch walk starts after the wait)
+  SegWalker pf_w0{};
   if (stashed) {
     if (warp == NC) {
       const int u0 = (int)cu0, u1 = (int)cu1;
@@ -1251,31 +1284,11 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
         int it0 = 0;
         pre_issued = produce_segment<D, NSTAGE>(p, tm, seg_ranges(p, s0), s0.b, s0.kvh, smem, full, empty, it0,
                                                 policy_evict_first(), s0.n, nullptr, 0, NSTAGE, true);
-        // the next MD_EARLY_PF full tiles of the CTA's units into L2 (a hint: safe whatever the
-        // previous kernel still writes -- L2 is the point of coherence), so the CTAs that become
-        // resident during the previous call's tail fill its idle HBM bandwidth with this call's reads
-        if (MD_EARLY_PF > 0 && lane == 0 && p.mode == MODE_DRAFT) {
-          int left = MD_EARLY_PF, skip = pre_issued;
-          Seg su = s0;
-          do {
-            const Ranges rg = seg_ranges(p, su);
-            for (int part = 0; part < 2 && left > 0; ++part) {
-              const int rs = part ? rg.s1 : rg.s0, re = part ? rg.e1 : rg.e0;
-              for (int pos = rs; pos + TK <= re && left > 0; pos += TK) {
-                if (skip > 0) {
-                  --skip;
-                  continue;
-                }
-                for (int sub = 0; sub < D / 64; ++sub) {
-                  tma_prefetch_4d(&tm.k_full, sub * 64, pos, su.kvh, su.b);
-                  tma_prefetch_4d(&tm.v_full, sub * 64, pos, su.kvh, su.b);
-                }
-                --left;
-              }
-            }
-            skip = 0;
-          } while (left > 0 && w0.next(p, pre, su));
-        }
+        // the next MD_EARLY_PF tiles into L2 while the previous call's tail leaves bandwidth idle
+        if (!MD_EPF_AFTER && MD_EARLY_PF > 0 && lane == 0 && p.mode == MODE_DRAFT)
+          early_l2_prefetch<D>(p, tm, pre, s0, w0, pre_issued);
+        pf_s0 = s0;
+        pf_w0 = w0;
       }
     }
   }
@@ -1286,6 +1299,7 @@ __global__ void __launch_bounds__(KeysCfg<D, KS, CTAS>::THREADS, CTAS)
     for (int j = 0; j < q0_ng * p.R; ++j)
       bulk_load(qbuf + j * C::QSTR, p.q + group_row(p, q0_unit, j) * D, D * 2, &qfull[0]);
     if (p.trace != nullptr) trace_put(p, 14, globaltimer());
+    if (MD_EPF_AFTER && MD_EARLY_PF > 0 && p.mode == MODE_DRAFT) early_l2_prefetch<D>(p, tm, pre, pf_s0, pf_w0, pre_issued);
   }
   // Unit-aligned plan (draft calls): CTA c owns the whole units [c*U/G, (c+1)*U/G), G = gridDim.x,
   // so it needs neither the per-sequence prefix table nor a plan -- its producer issues the
